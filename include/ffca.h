@@ -1,0 +1,162 @@
+/*
+ * ffca.h -- C ABI of the B200-native FastFCA-AS / FCA library (libffca_b200.so).
+ *
+ * The reference (fcasep, pure Python/numpy) has no FFI of its own; these entry
+ * points are what a ctypes / cffi binding of its hot-path Python functions
+ * binds.  Each declaration cites the reference function it replaces
+ * (paths relative to /root/reference/pkg/src/fcasep/).
+ *
+ * Conventions
+ *   - All arrays are C-contiguous in the REFERENCE layouts, with an extra
+ *     leading mixture axis U (U = 1 for a single mixture):
+ *       y    (U, I, N, F)  complex   stft.py:56-67 ObservationTensor.data
+ *       P    (U, F, I, I)  complex   fastfca.py:54
+ *       lam  (U, J, F, I)  real      fastfca.py:55
+ *       v    (U, J, N, F)  real      fastfca.py:56
+ *       S    (U, J, F, I, I) complex fca.py:34
+ *       mu   (U, J, N, F, I) complex  phi (U, J, N, F, I) real (fastfca.py:95-96)
+ *       images (U, J, I, N, F) complex  wiener.py:24
+ *   - dtype: FFCA_C128 (complex128 / float64, the reference's only path) or
+ *     FFCA_C64 (complex64 / float32).  Complex = interleaved (re, im).
+ *   - mem: FFCA_MEM_HOST -> every array pointer is host memory (the library
+ *     stages H2D / D2H itself); FFCA_MEM_DEVICE -> every array pointer is
+ *     device memory on `device` (no copies).  `stream` is a cudaStream_t
+ *     (NULL = legacy default stream); calls are stream-ordered and return
+ *     after completion.
+ *   - Return value 0 on success, otherwise an FFCA_E_* code; the message is
+ *     available from ffca_last_error().  Singularities are reported per bin
+ *     in `status` (FFCA_ST_* bits, (U, F) ints) when the pointer is given.
+ */
+#ifndef FFCA_H_
+#define FFCA_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FFCA_C128 0
+#define FFCA_C64 1
+
+#define FFCA_MEM_HOST 0
+#define FFCA_MEM_DEVICE 1
+
+/* v_floor modes (fastfca.py:406,421-424,435-436) */
+#define FFCA_VF_SCALAR 0 /* v_floor is a python float               */
+#define FFCA_VF_BIN 1    /* (U, F) array, e.g. fca.power_floor(obs) */
+#define FFCA_VF_FULL 2   /* (U, J, N, F) array                      */
+#define FFCA_VF_AUTO 3   /* v_floor=None: power_floor computed on device (fca.py:82-89) */
+
+#define FFCA_OK 0
+#define FFCA_E_ARG -1        /* bad sizes / pointers (errors.DimensionMismatch on the Python side) */
+#define FFCA_E_CUDA -2       /* CUDA runtime failure                                               */
+#define FFCA_E_SINGULAR_P -3 /* errors.SingularP                  fastfca.py:360-363, 268-271     */
+#define FFCA_E_SINGULAR_B -4 /* errors.SingularWeightedCovariance fastfca.py:184-194              */
+#define FFCA_E_NOT_PD -5     /* errors.NotPositiveDefinite        fca.py:137-140, 157-158         */
+#define FFCA_E_UNSUPPORTED -6 /* order I outside 1..8 (matcore.MAX_ORDER, matcore.py:20)           */
+
+#define FFCA_ST_SINGULAR_P 1
+#define FFCA_ST_SINGULAR_B 2
+#define FFCA_ST_B_LOADED 4
+#define FFCA_ST_NOT_PD 8
+#define FFCA_ST_S_LOADED 16
+
+/* Library / device info. */
+int ffca_version(void);
+const char* ffca_last_error(void);
+int ffca_device_count(void);
+/* Pinned host allocation helpers (for zero-staging H2D / D2H). */
+int ffca_host_alloc(void** ptr, long long bytes);
+int ffca_host_free(void* ptr);
+
+/*
+ * Hybrid FastFCA-AS loop: EM sweep on (v, lam) then fixed-point update of P,
+ * `iterations` times, all on device.  Replaces fastfca.run_fastfca
+ * (fastfca.py:401-474) minus the final stats refresh, which is
+ * ffca_fastfca_stats / ffca_fastfca_images below.
+ *   vf            scalar value for FFCA_VF_SCALAR, else array per vf_mode
+ *   ll_out        (U, 1 + 2*iterations) or NULL: [L_init, L_after_em[0..T-1], L_after_p[0..T-1]]
+ *                 (loglik_init / loglik_after_em / loglik_after_p, fastfca.py:448-459)
+ *   vf_out        (U, F) float64 or NULL: the floor used (auto mode)
+ *   P_out/lam_out/v_out may alias P0/lam0/v0.
+ */
+int ffca_fastfca_run(int device, void* stream, int mem, int dtype, int U, int I, int J, int N, int F,
+                     const void* y, const void* P0, const void* lam0, const void* v0, int vf_mode,
+                     double vf_scalar, const void* vf, int iterations, int inner_iterations,
+                     int record_likelihood, void* P_out, void* lam_out, void* v_out, double* ll_out,
+                     double* vf_out, int* status);
+
+/*
+ * Transformed posterior statistics at (P, lam, v): mu_t = g * P^H y and
+ * phi_t = max(a (1 - g), 0) with a = v lam, g = a / w.
+ * Replaces fastfca._stats_refresh (fastfca.py:373-387) and, given y_t,
+ * e_step_diag (fastfca.py:144-157).  mu / phi may be NULL (not produced).
+ */
+int ffca_fastfca_stats(int device, void* stream, int mem, int dtype, int U, int I, int J, int N, int F,
+                       const void* y, const void* P, const void* lam, const void* v, void* mu, void* phi);
+
+/*
+ * Multichannel Wiener images x_j = P^{-H} (g_j * P^H y), written (U, J, I, N, F).
+ * Fuses fastfca._stats_refresh + wiener.mmse_images_fastfca
+ * (fastfca.py:373-387, wiener.py:38-43, back_transform_means fastfca.py:258-273).
+ */
+int ffca_fastfca_images(int device, void* stream, int mem, int dtype, int U, int I, int J, int N, int F,
+                        const void* y, const void* P, const void* lam, const void* v, void* images,
+                        int* status);
+
+/*
+ * Solve P^H x = mu_t per bin for all (j, n): back_transform_means
+ * (fastfca.py:258-273).  mu_t (U, J, N, F, I) -> out (U, J, N, F, I); when
+ * `images_layout` != 0 the output is written (U, J, I, N, F) instead
+ * (wiener.mmse_images_fastfca, wiener.py:38-43).
+ */
+int ffca_back_transform(int device, void* stream, int mem, int dtype, int U, int I, int J, int N, int F,
+                        const void* P, const void* mu_t, void* out, int images_layout, int* status);
+
+/*
+ * Observed log likelihood L2 (fastfca.log_likelihood, fastfca.py:240-255),
+ * one value per mixture in ll_out (U,).
+ */
+int ffca_fastfca_loglik(int device, void* stream, int mem, int dtype, int U, int I, int J, int N, int F,
+                        const void* y, const void* P, const void* lam, const void* v, double* ll_out,
+                        int* status);
+
+/*
+ * Unfused fixed-point update of P (fastfca.fixed_point_update_P,
+ * fastfca.py:197-237): B_i from (y, v, lam) (hermitized), then K column
+ * updates.  P_out may alias P.
+ */
+int ffca_fixed_point_update_P(int device, void* stream, int mem, int dtype, int U, int I, int J, int N,
+                              int F, const void* y, const void* P, const void* lam, const void* v,
+                              int inner_iterations, void* P_out, int* status);
+
+/*
+ * Conventional FCA EM (fca.run_fca, fca.py:187-215).  S_prev / v_prev (may be
+ * NULL) receive the parameters of the last E-step (the returned stats are
+ * the E-step at those, fca.py:211).  ll_out (U, 1 + iterations) or NULL.
+ */
+int ffca_fca_run(int device, void* stream, int mem, int dtype, int U, int I, int J, int N, int F,
+                 const void* y, const void* S0, const void* v0, int vf_mode, double vf_scalar,
+                 const void* vf, int iterations, int record_likelihood, void* S_out, void* v_out,
+                 void* S_prev, void* v_prev, double* ll_out, int* status);
+
+/*
+ * Full-matrix E-step (fca.e_step, fca.py:119-144): mu (U,J,N,F,I) and phi
+ * (U,J,N,F,I,I); either may be NULL.  With images_layout != 0, mu is written
+ * (U, J, I, N, F) (wiener.mmse_images_fca, wiener.py:32-35).
+ */
+int ffca_fca_estep(int device, void* stream, int mem, int dtype, int U, int I, int J, int N, int F,
+                   const void* y, const void* S, const void* v, void* mu, void* phi, int images_layout,
+                   int* status);
+
+/* FCA observed log likelihood L1 (fca.log_likelihood, fca.py:101-116), (U,). */
+int ffca_fca_loglik(int device, void* stream, int mem, int dtype, int U, int I, int J, int N, int F,
+                    const void* y, const void* S, const void* v, double* ll_out, int* status);
+
+/* Kernel launches issued by the last successful call on this host thread. */
+int ffca_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FFCA_H_ */

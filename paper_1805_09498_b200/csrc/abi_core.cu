@@ -1,0 +1,104 @@
+// C-ABI core: error state, launch accounting, small shared device kernels.
+#include "host_common.h"
+
+#include <mutex>
+
+namespace ffca {
+
+static thread_local char g_err[1024] = {0};
+static thread_local int g_launches = 0;
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+void count_launch(int n) { g_launches += n; }
+void reset_launches() { g_launches = 0; }
+
+// Per-mixture likelihood totals: out[u*nev + e] = constant + sum_f part[(u*F + f)*nev + e],
+// summed in bin order (deterministic).
+__global__ void ll_reduce_kernel(const double* part, double* out, int U, int F, int nev, double constant) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= U * nev) return;
+  const int u = t / nev, e = t % nev;
+  double s = 0.0;
+  for (int f = 0; f < F; ++f) s += part[((long long)u * F + f) * nev + e];
+  out[t] = constant + s;
+}
+
+int reduce_ll(const double* ll_bins, double* ll_mix_dev, int U, int F, int nev, double constant,
+              cudaStream_t s) {
+  const int n = U * nev;
+  if (n == 0) return FFCA_OK;
+  ll_reduce_kernel<<<(n + 127) / 128, 128, 0, s>>>(ll_bins, ll_mix_dev, U, F, nev, constant);
+  count_launch();
+  FFCA_CK(cudaGetLastError());
+  return FFCA_OK;
+}
+
+int finish_status(const int* status_dev, int* status_user, long long nbins, int mem, cudaStream_t s,
+                  int fatal_mask) {
+  if (nbins == 0) return FFCA_OK;
+  std::vector<int> h(nbins);
+  FFCA_CK(cudaMemcpyAsync(h.data(), status_dev, nbins * sizeof(int), cudaMemcpyDeviceToHost, s));
+  FFCA_CK(cudaStreamSynchronize(s));
+  int any = 0;
+  long long first = -1;
+  for (long long k = 0; k < nbins; ++k) {
+    any |= h[k];
+    if (first < 0 && (h[k] & fatal_mask)) first = k;
+  }
+  if (status_user) {
+    if (mem == FFCA_MEM_DEVICE)
+      FFCA_CK(cudaMemcpyAsync(status_user, status_dev, nbins * sizeof(int), cudaMemcpyDeviceToDevice, s));
+    else
+      std::memcpy(status_user, h.data(), nbins * sizeof(int));
+  }
+  any &= fatal_mask;
+  if (any & FFCA_ST_SINGULAR_P) {
+    set_error("basis transform P is singular (bin index %lld)", first);
+    return FFCA_E_SINGULAR_P;
+  }
+  if (any & FFCA_ST_SINGULAR_B) {
+    set_error("weighted covariance stayed singular after diagonal loading (bin index %lld)", first);
+    return FFCA_E_SINGULAR_B;
+  }
+  if (any & FFCA_ST_NOT_PD) {
+    set_error("matrix not positive definite / singular (bin index %lld)", first);
+    return FFCA_E_NOT_PD;
+  }
+  return FFCA_OK;
+}
+
+}  // namespace ffca
+
+extern "C" {
+
+int ffca_version(void) { return 100; }
+
+const char* ffca_last_error(void) { return ffca::g_err; }
+
+int ffca_last_launch_count(void) { return ffca::g_launches; }
+
+int ffca_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int ffca_host_alloc(void** ptr, long long bytes) {
+  FFCA_CK(cudaMallocHost(ptr, size_t(bytes)));
+  return FFCA_OK;
+}
+
+int ffca_host_free(void* ptr) {
+  FFCA_CK(cudaFreeHost(ptr));
+  return FFCA_OK;
+}
+
+}  // extern "C"
