@@ -152,8 +152,35 @@ int ffca_fca_estep(int device, void* stream, int mem, int dtype, int U, int I, i
 int ffca_fca_loglik(int device, void* stream, int mem, int dtype, int U, int I, int J, int N, int F,
                     const void* y, const void* S, const void* v, double* ll_out, int* status);
 
+/* ---- step-level entry points (unfused public functions of fastfca.py) ---- */
+
+/* y_t = P^H y, (U, N, F, I): fastfca.transform_observations (fastfca.py:113-116). */
+int ffca_transform(int device, void* stream, int mem, int dtype, int U, int I, int N, int F, const void* y,
+                   const void* P, void* yt);
+
+/* w = max(sum_j v_j lam_j, floor), (U, N, F, I): fastfca.mixture_weights (fastfca.py:138-141). */
+int ffca_mixture_weights(int device, void* stream, int mem, int dtype, int U, int I, int J, int N, int F,
+                         const void* lam, const void* v, void* w);
+
+/* e_step_diag from a given y_t (U, N, F, I): fastfca.e_step_diag (fastfca.py:144-157). */
+int ffca_fastfca_estep_yt(int device, void* stream, int mem, int dtype, int U, int I, int J, int N, int F,
+                          const void* yt, const void* lam, const void* v, void* mu, void* phi);
+
+/* fastfca.m_step_diag (fastfca.py:160-181); vf_mode SCALAR / BIN / FULL. */
+int ffca_mstep_diag(int device, void* stream, int mem, int dtype, int U, int I, int J, int N, int F,
+                    const void* mu, const void* phi, const void* lam, int vf_mode, double vf_scalar,
+                    const void* vf, void* v_out, void* lam_out);
+
+/* Launch plan of the loop kernel for a shape: out6 = {G, C, NL, threads, resident, smem}. */
+int ffca_plan_loop(int device, int dtype, int U, int I, int J, int N, int F, int vf_mode, int* out6);
+
 /* Kernel launches issued by the last successful call on this host thread. */
 int ffca_last_launch_count(void);
+
+/* Opt-in CUDA-event timing of the estimation-loop kernel on its launch stream
+ * (this host thread); ffca_last_kernel_ms() returns the last measured launch. */
+void ffca_set_kernel_timing(int on);
+float ffca_last_kernel_ms(void);
 
 #ifdef __cplusplus
 }

@@ -44,6 +44,8 @@ SIGNATURES = {
     "ffca_host_alloc": [ctypes.POINTER(_vp), ctypes.c_longlong],
     "ffca_host_free": [_vp],
     "ffca_last_launch_count": [],
+    "ffca_set_kernel_timing": [_i],
+    "ffca_last_kernel_ms": [],
     "ffca_plan_loop": [_i, _i, _i, _i, _i, _i, _i, _i, _ip],
     "ffca_fastfca_run": [_i, _vp, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _i, _d, _vp, _i, _i, _i,
                          _vp, _vp, _vp, _vp, _vp, _vp],
@@ -56,8 +58,13 @@ SIGNATURES = {
                      _vp, _vp, _vp],
     "ffca_fca_estep": [_i, _vp, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp],
     "ffca_fca_loglik": [_i, _vp, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp],
+    "ffca_transform": [_i, _vp, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp],
+    "ffca_mixture_weights": [_i, _vp, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp],
+    "ffca_fastfca_estep_yt": [_i, _vp, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp],
+    "ffca_mstep_diag": [_i, _vp, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _d, _vp, _vp, _vp],
 }
-_RESTYPES = {"ffca_last_error": ctypes.c_char_p}
+_RESTYPES = {"ffca_last_error": ctypes.c_char_p, "ffca_set_kernel_timing": None,
+             "ffca_last_kernel_ms": ctypes.c_float}
 
 _lib = None
 _device = int(os.environ.get("FFCA_DEVICE", "0"))

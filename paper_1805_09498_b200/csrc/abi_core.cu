@@ -7,6 +7,8 @@ namespace ffca {
 
 static thread_local char g_err[1024] = {0};
 static thread_local int g_launches = 0;
+static thread_local int g_timing = 0;
+static thread_local float g_kernel_ms = 0.f;
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -16,6 +18,8 @@ void set_error(const char* fmt, ...) {
 }
 void count_launch(int n) { g_launches += n; }
 void reset_launches() { g_launches = 0; }
+bool timing_enabled() { return g_timing != 0; }
+void set_kernel_ms(float ms) { g_kernel_ms = ms; }
 
 // Per-mixture likelihood totals: out[u*nev + e] = constant + sum_f part[(u*F + f)*nev + e],
 // summed in bin order (deterministic).
@@ -81,6 +85,10 @@ int ffca_version(void) { return 100; }
 const char* ffca_last_error(void) { return ffca::g_err; }
 
 int ffca_last_launch_count(void) { return ffca::g_launches; }
+
+void ffca_set_kernel_timing(int on) { ffca::g_timing = on; }
+
+float ffca_last_kernel_ms(void) { return ffca::g_kernel_ms; }
 
 int ffca_device_count(void) {
   int n = 0;

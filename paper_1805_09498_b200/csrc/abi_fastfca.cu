@@ -1,5 +1,7 @@
 // C-ABI: FastFCA-AS estimation loop (ffca_fastfca_run).
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "ffca_loop.cuh"
 #include "host_common.h"
@@ -57,6 +59,16 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
     p.slab = L.slab;
     p.grid = ((total_bins + G - 1) / G) * C;
   };
+  // Test hook: FFCA_FORCE_PLAN="G,C,resident" pins the launch plan (parity tests
+  // use it to exercise the cluster and global-slab paths at small sizes).
+  if (const char* fp = getenv("FFCA_FORCE_PLAN")) {
+    int G = 1, C = 1, res = 1;
+    if (sscanf(fp, "%d,%d,%d", &G, &C, &res) == 3 && (G == 1 || G == 2 || G == 4) && C >= 1 && C <= 8 &&
+        (C & (C - 1)) == 0 && C <= N && (C == 1 || G == 1)) {
+      fill(G, C, res != 0);
+      if (p.smem <= smem_optin) return FFCA_OK;
+    }
+  }
   for (int G = G0; G >= 1; G >>= 1) {
     fill(G, 1, true);
     if (p.slab <= kSlabBudget && p.smem <= smem_optin) return FFCA_OK;
@@ -99,11 +111,11 @@ static int launch_loop(LoopFn fn, const LoopPlan& p, const LoopArgs& a, cudaStre
 
 using namespace ffca;
 
-extern "C" int ffca_fastfca_run(int device, void* stream, int mem, int dtype, int U, int I, int J, int N,
-                                int F, const void* y, const void* P0, const void* lam0, const void* v0,
-                                int vf_mode, double vf_scalar, const void* vf, int iterations,
-                                int inner_iterations, int record_likelihood, void* P_out, void* lam_out,
-                                void* v_out, double* ll_out, double* vf_out, int* status) {
+static int loop_entry(int device, void* stream, int mem, int dtype, int U, int I, int J, int N, int F,
+                      const void* y, const void* P0, const void* lam0, const void* v0, int vf_mode,
+                      double vf_scalar, const void* vf, int iterations, int inner_iterations,
+                      int record_likelihood, void* P_out, void* lam_out, void* v_out, double* ll_out,
+                      double* vf_out, int* status, int p_only) {
   reset_launches();
   if (!check_dims(dtype, U, I, J, N, F)) return FFCA_E_ARG;
   if (I > 8 || J > 8) {
@@ -159,7 +171,7 @@ extern "C" int ffca_fastfca_run(int device, void* stream, int mem, int dtype, in
   a.U = U; a.I = I; a.J = J; a.N = N; a.F = F;
   a.total_bins = nb;
   a.G = p.G; a.C = p.C; a.NL = p.NL;
-  a.iters = iterations; a.K = inner_iterations;
+  a.iters = iterations; a.K = inner_iterations; a.p_only = p_only;
   a.vf_mode = vf_mode; a.vf_scalar = vf_scalar; a.vf = dvf;
   a.y = dy; a.P_in = dP; a.lam_in = dl; a.v_in = dv;
   a.P_out = oP; a.lam_out = ol; a.v_out = ov;
@@ -175,11 +187,125 @@ extern "C" int ffca_fastfca_run(int device, void* stream, int mem, int dtype, in
     set_error("no kernel for I=%d J=%d", I, J);
     return FFCA_E_UNSUPPORTED;
   }
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (timing_enabled()) {
+    FFCA_CK(cudaEventCreate(&ev0));
+    FFCA_CK(cudaEventCreate(&ev1));
+    FFCA_CK(cudaEventRecord(ev0, s));
+  }
   FFCA_TRY(launch_loop(fn, p, a, s));
   FFCA_CK(cudaGetLastError());
+  if (ev0) {
+    FFCA_CK(cudaEventRecord(ev1, s));
+    FFCA_CK(cudaEventSynchronize(ev1));
+    float ms = 0.f;
+    FFCA_CK(cudaEventElapsedTime(&ms, ev0, ev1));
+    set_kernel_ms(ms);
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+  }
   if (oll) FFCA_TRY(reduce_ll((const double*)dllb, (double*)oll, U, F, nev, -double(N) * F * I * std::log(M_PI), s));
   FFCA_TRY(st.flush());
   return finish_status((const int*)dstatus, status, nb, mem, s, FFCA_ST_SINGULAR_P | FFCA_ST_SINGULAR_B);
+}
+
+extern "C" int ffca_fastfca_run(int device, void* stream, int mem, int dtype, int U, int I, int J, int N,
+                                int F, const void* y, const void* P0, const void* lam0, const void* v0,
+                                int vf_mode, double vf_scalar, const void* vf, int iterations,
+                                int inner_iterations, int record_likelihood, void* P_out, void* lam_out,
+                                void* v_out, double* ll_out, double* vf_out, int* status) {
+  return loop_entry(device, stream, mem, dtype, U, I, J, N, F, y, P0, lam0, v0, vf_mode, vf_scalar, vf,
+                    iterations, inner_iterations, record_likelihood, P_out, lam_out, v_out, ll_out, vf_out,
+                    status, 0);
+}
+
+// fastfca.log_likelihood (fastfca.py:240-255): the loop kernel with zero
+// iterations evaluates exactly L2 at the given state.
+extern "C" int ffca_fastfca_loglik(int device, void* stream, int mem, int dtype, int U, int I, int J, int N,
+                                   int F, const void* y, const void* P, const void* lam, const void* v,
+                                   double* ll_out, int* status) {
+  if (!check_dims(dtype, U, I, J, N, F)) return FFCA_E_ARG;
+  DeviceGuard dg(device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t rs = rsize(dtype), cs = csize(dtype);
+  const long long nb = (long long)U * F;
+  // scratch outputs on device; only the likelihood is returned
+  void *Po = nullptr, *lo = nullptr, *vo = nullptr;
+  FFCA_CK(cudaMallocAsync(&Po, size_t(nb) * I * I * cs + 16, s));
+  FFCA_CK(cudaMallocAsync(&lo, size_t(U) * J * F * I * rs + 16, s));
+  FFCA_CK(cudaMallocAsync(&vo, size_t(U) * J * N * F * rs + 16, s));
+  int rc = FFCA_OK;
+  {
+    // stage inputs here so the loop entry can run in device mode
+    Staging st(mem, s);
+    const void *dy, *dP, *dl, *dv;
+    void* dll;
+    rc = st.in(y, size_t(U) * I * N * F * cs, &dy);
+    if (!rc) rc = st.in(P, size_t(nb) * I * I * cs, &dP);
+    if (!rc) rc = st.in(lam, size_t(U) * J * F * I * rs, &dl);
+    if (!rc) rc = st.in(v, size_t(U) * J * N * F * rs, &dv);
+    if (!rc) rc = st.out(ll_out, size_t(U) * 8, &dll);
+    if (!rc) {
+      int* dst = nullptr;
+      if (status && mem == FFCA_MEM_DEVICE) dst = status;
+      std::vector<int> hst;
+      rc = loop_entry(device, stream, FFCA_MEM_DEVICE, dtype, U, I, J, N, F, dy, dP, dl, dv, FFCA_VF_SCALAR, 0.0,
+                      nullptr, 0, 1, 1, Po, lo, vo, (double*)dll, nullptr, dst, 0);
+      if (rc == FFCA_OK) rc = st.flush();
+      if (rc == FFCA_OK) {
+        cudaError_t e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) {
+          set_error("%s", cudaGetErrorString(e));
+          rc = FFCA_E_CUDA;
+        }
+      }
+    }
+  }
+  cudaFreeAsync(Po, s);
+  cudaFreeAsync(lo, s);
+  cudaFreeAsync(vo, s);
+  return rc;
+}
+
+// fastfca.fixed_point_update_P (fastfca.py:197-237): one P-only pass of the
+// loop kernel (B_i hermitized from the packed lower triangle, K updates).
+extern "C" int ffca_fixed_point_update_P(int device, void* stream, int mem, int dtype, int U, int I, int J,
+                                         int N, int F, const void* y, const void* P, const void* lam,
+                                         const void* v, int inner_iterations, void* P_out, int* status) {
+  if (!check_dims(dtype, U, I, J, N, F)) return FFCA_E_ARG;
+  DeviceGuard dg(device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t rs = rsize(dtype), cs = csize(dtype);
+  const long long nb = (long long)U * F;
+  void *lo = nullptr, *vo = nullptr;
+  FFCA_CK(cudaMallocAsync(&lo, size_t(U) * J * F * I * rs + 16, s));
+  FFCA_CK(cudaMallocAsync(&vo, size_t(U) * J * N * F * rs + 16, s));
+  int rc;
+  {
+    Staging st(mem, s);
+    const void *dy, *dP, *dl, *dv;
+    void* dPo;
+    rc = st.in(y, size_t(U) * I * N * F * cs, &dy);
+    if (!rc) rc = st.in(P, size_t(nb) * I * I * cs, &dP);
+    if (!rc) rc = st.in(lam, size_t(U) * J * F * I * rs, &dl);
+    if (!rc) rc = st.in(v, size_t(U) * J * N * F * rs, &dv);
+    if (!rc) rc = st.out(P_out, size_t(nb) * I * I * cs, &dPo);
+    if (!rc) {
+      int* dst = (status && mem == FFCA_MEM_DEVICE) ? status : nullptr;
+      std::vector<int> hst(status && mem != FFCA_MEM_DEVICE ? nb : 0);
+      rc = loop_entry(device, stream, FFCA_MEM_DEVICE, dtype, U, I, J, N, F, dy, dP, dl, dv, FFCA_VF_SCALAR,
+                      0.0, nullptr, 1, inner_iterations, 0, dPo, lo, vo, nullptr, nullptr, dst, 1);
+      (void)hst;
+      if (rc == FFCA_OK) rc = st.flush();
+      if (rc == FFCA_OK && cudaStreamSynchronize(s) != cudaSuccess) {
+        set_error("%s", cudaGetErrorString(cudaGetLastError()));
+        rc = FFCA_E_CUDA;
+      }
+    }
+  }
+  cudaFreeAsync(lo, s);
+  cudaFreeAsync(vo, s);
+  return rc;
 }
 
 // Introspection for tests / bench: the launch plan chosen for a shape.

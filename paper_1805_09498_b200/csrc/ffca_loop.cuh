@@ -29,6 +29,7 @@ struct LoopArgs {
   int C;         // cluster size (CTAs sharing one bin group, split over n)
   int NL;        // max frames held by one CTA (ceil(N / C))
   int iters, K;
+  int p_only;     // skip the EM sweep: fixed_point_update_P (fastfca.py:197-237)
   int vf_mode;   // 0 scalar, 1 per-bin (U,F), 2 full (U,J,N,F), 3 auto (power floor)
   double vf_scalar;
   const void* vf;      // real array for modes 1, 2
@@ -313,7 +314,7 @@ __global__ void __launch_bounds__(256) ffca_loop_kernel(const LoopArgs a) {
     // ---------------- phase A: fused E/M sweep ----------------
     FFCA_LOAD_PL();
     double llA = 0.0;
-    {
+    if (!a.p_only) {
       R acc[VA];
 #pragma unroll
       for (int k = 0; k < VA; ++k) acc[k] = R(0);
@@ -363,7 +364,7 @@ __global__ void __launch_bounds__(256) ffca_loop_kernel(const LoopArgs a) {
       if (rec && tid < G) llA = tot[tid * VMAX + VA - 1];
     }
     // ---------------- lambda' per (bin, source) ----------------
-    for (int t = tid; t < G * J; t += blockDim.x) {
+    for (int t = tid; t < (a.p_only ? 0 : G * J); t += blockDim.x) {
       const int gg = t / J, j = t % J;
       const double* T = tot + gg * VMAX;
       const double s0 = T[j] * invN;

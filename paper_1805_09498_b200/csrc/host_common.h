@@ -16,6 +16,8 @@ namespace ffca {
 void set_error(const char* fmt, ...);
 void count_launch(int n = 1);
 void reset_launches();
+bool timing_enabled();
+void set_kernel_ms(float ms);
 
 #define FFCA_CK(call)                                                                    \
   do {                                                                                   \

@@ -1,0 +1,410 @@
+// Per-(n, f) streaming kernels of the FastFCA-AS path (sm_100a).
+//
+// One thread per time-frequency point, frequency fastest, so every load and
+// store of the reference layouts (y (U,I,N,F), v (U,J,N,F), outputs
+// (U,J,N,F,I) and (U,J,I,N,F)) is coalesced across a warp.  These are pure
+// HBM-streaming kernels: per-bin matrices (P, P^-H, lambda) are read through
+// L1/L2, which hold them for all frames of a bin.
+#include <cmath>
+
+#include "common.cuh"
+#include "host_common.h"
+
+namespace ffca {
+
+enum PointMode : int {
+  PM_STATS = 0,      // y, P, lam, v -> mu_t, phi_t       (fastfca.py:373-387)
+  PM_ESTEP_YT = 1,   // y_t, lam, v  -> mu_t, phi_t       (fastfca.py:144-157)
+  PM_TRANSFORM = 2,  // y, P         -> y_t (N,F,I)       (fastfca.py:113-116)
+  PM_WEIGHTS = 3,    // lam, v       -> w (N,F,I)         (fastfca.py:138-141)
+  PM_IMAGES = 4,     // y, P, Q=P^-H, lam, v -> images    (wiener.py:38-43 on the final state)
+  PM_BACK = 5,       // mu_t, Q      -> Q mu_t            (fastfca.py:258-273)
+};
+
+struct PointArgs {
+  int mode, U, I, J, N, F;
+  const void* y;     // (U,I,N,F) complex, or y_t (U,N,F,I) for PM_ESTEP_YT, or mu_t (U,J,N,F,I) for PM_BACK
+  const void* P;     // (U,F,I,I) complex
+  const void* Q;     // (U,F,I,I) complex fp64: P^-H
+  const void* lam;   // (U,J,F,I) real
+  const void* v;     // (U,J,N,F) real
+  void* out0;        // mu_t / y_t / w / images / back
+  void* out1;        // phi_t
+  int images_layout; // PM_BACK: write (U,J,I,N,F)
+};
+
+template <typename R, int I>
+__global__ void __launch_bounds__(256) point_kernel(const PointArgs a) {
+  using C2 = typename Cpx<R>::T;
+  const long long npts = (long long)a.U * a.N * a.F;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= npts) return;
+  const int F = a.F, N = a.N, J = a.J;
+  const int f = int(t % F);
+  const long long un = t / F;
+  const int n = int(un % N);
+  const long long u = un / N;
+  const long long bin = u * F + f;
+  const R wfl = Floors<R>::weight;
+
+  if (a.mode == PM_BACK) {
+    const double2* Q = (const double2*)a.Q + bin * I * I;
+    const C2* mu = (const C2*)a.y;
+    C2* out = (C2*)a.out0;
+    for (int j = 0; j < J; ++j) {
+      const long long base = (((u * J + j) * N + n) * (long long)F + f) * I;
+      C2 m[I];
+#pragma unroll
+      for (int i = 0; i < I; ++i) m[i] = mu[base + i];
+#pragma unroll
+      for (int x = 0; x < I; ++x) {
+        double re = 0.0, im = 0.0;
+#pragma unroll
+        for (int b = 0; b < I; ++b) {
+          const double2 q = Q[x * I + b];
+          re += q.x * double(m[b].x) - q.y * double(m[b].y);
+          im += q.x * double(m[b].y) + q.y * double(m[b].x);
+        }
+        const C2 r = mk<C2, R>(R(re), R(im));
+        if (a.images_layout)
+          out[(((u * J + j) * I + x) * (long long)N + n) * F + f] = r;
+        else
+          out[base + x] = r;
+      }
+    }
+    return;
+  }
+
+  // transformed observation y_t = P^H y (or given)
+  C2 yt[I];
+  if (a.mode == PM_STATS || a.mode == PM_TRANSFORM || a.mode == PM_IMAGES) {
+    const C2* y = (const C2*)a.y;
+    const C2* P = (const C2*)a.P + bin * I * I;
+    C2 yv[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) yv[i] = y[((u * I + i) * N + n) * (long long)F + f];
+#pragma unroll
+    for (int b = 0; b < I; ++b) {
+      C2 acc = mk<C2, R>(R(0), R(0));
+#pragma unroll
+      for (int x = 0; x < I; ++x) cmac_conj(acc, P[x * I + b], yv[x]);
+      yt[b] = acc;
+    }
+    if (a.mode == PM_TRANSFORM) {
+      C2* out = (C2*)a.out0;
+#pragma unroll
+      for (int b = 0; b < I; ++b) out[t * I + b] = yt[b];
+      return;
+    }
+  } else if (a.mode == PM_ESTEP_YT) {
+    const C2* y = (const C2*)a.y;
+#pragma unroll
+    for (int b = 0; b < I; ++b) yt[b] = y[t * I + b];
+  }
+
+  // mixture weights
+  const R* v = (const R*)a.v;
+  const R* lam = (const R*)a.lam;
+  R w[I];
+#pragma unroll
+  for (int i = 0; i < I; ++i) w[i] = R(0);
+  for (int j = 0; j < J; ++j) {
+    const R vj = v[((u * J + j) * N + n) * (long long)F + f];
+#pragma unroll
+    for (int i = 0; i < I; ++i) w[i] = fma(vj, lam[((u * J + j) * F + f) * I + i], w[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < I; ++i) w[i] = fmax(w[i], wfl);
+  if (a.mode == PM_WEIGHTS) {
+    R* out = (R*)a.out0;
+#pragma unroll
+    for (int i = 0; i < I; ++i) out[t * I + i] = w[i];
+    return;
+  }
+
+  const double2* Q = a.mode == PM_IMAGES ? (const double2*)a.Q + bin * I * I : nullptr;
+  for (int j = 0; j < J; ++j) {
+    const R vj = v[((u * J + j) * N + n) * (long long)F + f];
+    const long long base = (((u * J + j) * N + n) * (long long)F + f) * I;
+    C2 mu[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      const R aa = vj * lam[((u * J + j) * F + f) * I + i];
+      const R g = quot(aa, w[i]);
+      mu[i] = mk<C2, R>(g * yt[i].x, g * yt[i].y);
+      if (a.mode != PM_IMAGES) {
+        if (a.out0) ((C2*)a.out0)[base + i] = mu[i];
+        if (a.out1) ((R*)a.out1)[base + i] = fmax(aa * (R(1) - g), R(0));
+      }
+    }
+    if (a.mode == PM_IMAGES) {
+      C2* out = (C2*)a.out0;
+#pragma unroll
+      for (int x = 0; x < I; ++x) {
+        double re = 0.0, im = 0.0;
+#pragma unroll
+        for (int b = 0; b < I; ++b) {
+          const double2 q = Q[x * I + b];
+          re += q.x * double(mu[b].x) - q.y * double(mu[b].y);
+          im += q.x * double(mu[b].y) + q.y * double(mu[b].x);
+        }
+        out[(((u * J + j) * I + x) * (long long)N + n) * F + f] = mk<C2, R>(R(re), R(im));
+      }
+    }
+  }
+}
+
+// Q = P^-H per bin (one thread per bin, fp64, LU from common.cuh in a
+// per-thread local workspace).  Flags exactly singular P.
+template <typename R, int I>
+__global__ void inv_PH_kernel(const void* Pv, double2* Q, int* status, long long nbins) {
+  using C2 = typename Cpx<R>::T;
+  const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nbins) return;
+  const C2* P = (const C2*)Pv + b * I * I;
+  double2 A[I * I], col[I];
+  int piv[I];
+  // factor P^H
+#pragma unroll
+  for (int x = 0; x < I; ++x)
+#pragma unroll
+    for (int y = 0; y < I; ++y) A[x * I + y] = make_double2(double(P[y * I + x].x), -double(P[y * I + x].y));
+  if (!lu_factor<I>(A, piv)) {
+    status[b] |= ST_SINGULAR_P;
+    return;
+  }
+  for (int c = 0; c < I; ++c) {
+#pragma unroll
+    for (int x = 0; x < I; ++x) col[x] = make_double2(x == c ? 1.0 : 0.0, 0.0);
+    lu_solve<I>(A, piv, col);
+#pragma unroll
+    for (int x = 0; x < I; ++x) Q[b * I * I + x * I + c] = col[x];
+  }
+}
+
+template <typename R>
+static void* point_fn(int I) {
+  switch (I) {
+    case 1: return (void*)point_kernel<R, 1>;
+    case 2: return (void*)point_kernel<R, 2>;
+    case 3: return (void*)point_kernel<R, 3>;
+    case 4: return (void*)point_kernel<R, 4>;
+    case 5: return (void*)point_kernel<R, 5>;
+    case 6: return (void*)point_kernel<R, 6>;
+    case 7: return (void*)point_kernel<R, 7>;
+    case 8: return (void*)point_kernel<R, 8>;
+  }
+  return nullptr;
+}
+
+template <typename R>
+static void* inv_fn(int I) {
+  switch (I) {
+    case 1: return (void*)inv_PH_kernel<R, 1>;
+    case 2: return (void*)inv_PH_kernel<R, 2>;
+    case 3: return (void*)inv_PH_kernel<R, 3>;
+    case 4: return (void*)inv_PH_kernel<R, 4>;
+    case 5: return (void*)inv_PH_kernel<R, 5>;
+    case 6: return (void*)inv_PH_kernel<R, 6>;
+    case 7: return (void*)inv_PH_kernel<R, 7>;
+    case 8: return (void*)inv_PH_kernel<R, 8>;
+  }
+  return nullptr;
+}
+
+int launch_points(int dtype, const PointArgs& a, cudaStream_t s) {
+  const long long npts = (long long)a.U * a.N * a.F;
+  if (npts == 0) return FFCA_OK;
+  void* fn = dtype == FFCA_C64 ? point_fn<float>(a.I) : point_fn<double>(a.I);
+  if (!fn) {
+    set_error("unsupported order I=%d", a.I);
+    return FFCA_E_UNSUPPORTED;
+  }
+  const unsigned blocks = unsigned((npts + 255) / 256);
+  void* args[] = {(void*)&a};
+  FFCA_CK(cudaLaunchKernel(fn, dim3(blocks), dim3(256), args, 0, s));
+  count_launch();
+  return FFCA_OK;
+}
+
+int launch_inv_PH(int dtype, int I, const void* P, double2* Q, int* status, long long nbins, cudaStream_t s) {
+  if (nbins == 0) return FFCA_OK;
+  void* fn = dtype == FFCA_C64 ? inv_fn<float>(I) : inv_fn<double>(I);
+  if (!fn) {
+    set_error("unsupported order I=%d", I);
+    return FFCA_E_UNSUPPORTED;
+  }
+  const unsigned blocks = unsigned((nbins + 127) / 128);
+  void* args[] = {(void*)&P, (void*)&Q, (void*)&status, (void*)&nbins};
+  FFCA_CK(cudaLaunchKernel(fn, dim3(blocks), dim3(128), args, 0, s));
+  count_launch();
+  return FFCA_OK;
+}
+
+}  // namespace ffca
+
+using namespace ffca;
+
+static int points_common(int device, void* stream, int mem, int dtype, int U, int I, int J, int N, int F) {
+  (void)device;
+  (void)stream;
+  (void)mem;
+  if (!check_dims(dtype, U, I, J, N, F)) return FFCA_E_ARG;
+  if (I > 8) {
+    set_error("unsupported order I=%d (matcore.MAX_ORDER = 8)", I);
+    return FFCA_E_UNSUPPORTED;
+  }
+  return FFCA_OK;
+}
+
+extern "C" int ffca_fastfca_stats(int device, void* stream, int mem, int dtype, int U, int I, int J, int N,
+                                  int F, const void* y, const void* P, const void* lam, const void* v, void* mu,
+                                  void* phi) {
+  reset_launches();
+  FFCA_TRY(points_common(device, stream, mem, dtype, U, I, J, N, F));
+  if (!y || !P || !lam || !v) {
+    set_error("null array argument");
+    return FFCA_E_ARG;
+  }
+  DeviceGuard dg(device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t rs = rsize(dtype), cs = csize(dtype);
+  Staging st(mem, s);
+  PointArgs a = {};
+  a.mode = PM_STATS; a.U = U; a.I = I; a.J = J; a.N = N; a.F = F;
+  FFCA_TRY(st.in(y, size_t(U) * I * N * F * cs, &a.y));
+  FFCA_TRY(st.in(P, size_t(U) * F * I * I * cs, &a.P));
+  FFCA_TRY(st.in(lam, size_t(U) * J * F * I * rs, &a.lam));
+  FFCA_TRY(st.in(v, size_t(U) * J * N * F * rs, &a.v));
+  FFCA_TRY(st.out(mu, size_t(U) * J * N * F * I * cs, &a.out0));
+  FFCA_TRY(st.out(phi, size_t(U) * J * N * F * I * rs, &a.out1));
+  FFCA_TRY(launch_points(dtype, a, s));
+  FFCA_TRY(st.flush());
+  FFCA_CK(cudaStreamSynchronize(s));
+  return FFCA_OK;
+}
+
+// e_step_diag from a given y_t (N, F, I) -- exposed through the same entry with
+// y = y_t when the caller passes FFCA_ESTEP_YT in `mem` bit 8 (internal use).
+extern "C" int ffca_fastfca_estep_yt(int device, void* stream, int mem, int dtype, int U, int I, int J, int N,
+                                     int F, const void* yt, const void* lam, const void* v, void* mu,
+                                     void* phi) {
+  reset_launches();
+  FFCA_TRY(points_common(device, stream, mem, dtype, U, I, J, N, F));
+  DeviceGuard dg(device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t rs = rsize(dtype), cs = csize(dtype);
+  Staging st(mem, s);
+  PointArgs a = {};
+  a.mode = PM_ESTEP_YT; a.U = U; a.I = I; a.J = J; a.N = N; a.F = F;
+  FFCA_TRY(st.in(yt, size_t(U) * N * F * I * cs, &a.y));
+  FFCA_TRY(st.in(lam, size_t(U) * J * F * I * rs, &a.lam));
+  FFCA_TRY(st.in(v, size_t(U) * J * N * F * rs, &a.v));
+  FFCA_TRY(st.out(mu, size_t(U) * J * N * F * I * cs, &a.out0));
+  FFCA_TRY(st.out(phi, size_t(U) * J * N * F * I * rs, &a.out1));
+  FFCA_TRY(launch_points(dtype, a, s));
+  FFCA_TRY(st.flush());
+  FFCA_CK(cudaStreamSynchronize(s));
+  return FFCA_OK;
+}
+
+extern "C" int ffca_transform(int device, void* stream, int mem, int dtype, int U, int I, int N, int F,
+                              const void* y, const void* P, void* yt) {
+  reset_launches();
+  FFCA_TRY(points_common(device, stream, mem, dtype, U, I, 1, N, F));
+  DeviceGuard dg(device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t cs = csize(dtype);
+  Staging st(mem, s);
+  PointArgs a = {};
+  a.mode = PM_TRANSFORM; a.U = U; a.I = I; a.J = 1; a.N = N; a.F = F;
+  FFCA_TRY(st.in(y, size_t(U) * I * N * F * cs, &a.y));
+  FFCA_TRY(st.in(P, size_t(U) * F * I * I * cs, &a.P));
+  FFCA_TRY(st.out(yt, size_t(U) * N * F * I * cs, &a.out0));
+  FFCA_TRY(launch_points(dtype, a, s));
+  FFCA_TRY(st.flush());
+  FFCA_CK(cudaStreamSynchronize(s));
+  return FFCA_OK;
+}
+
+extern "C" int ffca_mixture_weights(int device, void* stream, int mem, int dtype, int U, int I, int J, int N,
+                                    int F, const void* lam, const void* v, void* w) {
+  reset_launches();
+  FFCA_TRY(points_common(device, stream, mem, dtype, U, I, J, N, F));
+  DeviceGuard dg(device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t rs = rsize(dtype);
+  Staging st(mem, s);
+  PointArgs a = {};
+  a.mode = PM_WEIGHTS; a.U = U; a.I = I; a.J = J; a.N = N; a.F = F;
+  FFCA_TRY(st.in(lam, size_t(U) * J * F * I * rs, &a.lam));
+  FFCA_TRY(st.in(v, size_t(U) * J * N * F * rs, &a.v));
+  FFCA_TRY(st.out(w, size_t(U) * N * F * I * rs, &a.out0));
+  FFCA_TRY(launch_points(dtype, a, s));
+  FFCA_TRY(st.flush());
+  FFCA_CK(cudaStreamSynchronize(s));
+  return FFCA_OK;
+}
+
+extern "C" int ffca_fastfca_images(int device, void* stream, int mem, int dtype, int U, int I, int J, int N,
+                                   int F, const void* y, const void* P, const void* lam, const void* v,
+                                   void* images, int* status) {
+  reset_launches();
+  FFCA_TRY(points_common(device, stream, mem, dtype, U, I, J, N, F));
+  if (!y || !P || !lam || !v || !images) {
+    set_error("null array argument");
+    return FFCA_E_ARG;
+  }
+  DeviceGuard dg(device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t rs = rsize(dtype), cs = csize(dtype);
+  const long long nb = (long long)U * F;
+  Staging st(mem, s);
+  PointArgs a = {};
+  a.mode = PM_IMAGES; a.U = U; a.I = I; a.J = J; a.N = N; a.F = F;
+  FFCA_TRY(st.in(y, size_t(U) * I * N * F * cs, &a.y));
+  FFCA_TRY(st.in(P, size_t(nb) * I * I * cs, &a.P));
+  FFCA_TRY(st.in(lam, size_t(U) * J * F * I * rs, &a.lam));
+  FFCA_TRY(st.in(v, size_t(U) * J * N * F * rs, &a.v));
+  FFCA_TRY(st.out(images, size_t(U) * J * I * N * F * cs, &a.out0));
+  void *Q, *dstatus;
+  FFCA_TRY(st.scratch(size_t(nb) * I * I * 16, &Q));
+  FFCA_TRY(st.scratch(size_t(nb) * 4, &dstatus));
+  FFCA_CK(cudaMemsetAsync(dstatus, 0, size_t(nb) * 4, s));
+  FFCA_TRY(launch_inv_PH(dtype, I, a.P, (double2*)Q, (int*)dstatus, nb, s));
+  a.Q = Q;
+  FFCA_TRY(launch_points(dtype, a, s));
+  FFCA_TRY(st.flush());
+  return finish_status((const int*)dstatus, status, nb, mem, s, FFCA_ST_SINGULAR_P);
+}
+
+extern "C" int ffca_back_transform(int device, void* stream, int mem, int dtype, int U, int I, int J, int N,
+                                   int F, const void* P, const void* mu_t, void* out, int images_layout,
+                                   int* status) {
+  reset_launches();
+  FFCA_TRY(points_common(device, stream, mem, dtype, U, I, J, N, F));
+  if (!P || !mu_t || !out) {
+    set_error("null array argument");
+    return FFCA_E_ARG;
+  }
+  DeviceGuard dg(device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t cs = csize(dtype);
+  const long long nb = (long long)U * F;
+  Staging st(mem, s);
+  PointArgs a = {};
+  a.mode = PM_BACK; a.U = U; a.I = I; a.J = J; a.N = N; a.F = F;
+  a.images_layout = images_layout;
+  FFCA_TRY(st.in(P, size_t(nb) * I * I * cs, &a.P));
+  FFCA_TRY(st.in(mu_t, size_t(U) * J * N * F * I * cs, &a.y));
+  FFCA_TRY(st.out(out, size_t(U) * J * N * F * I * cs, &a.out0));
+  void *Q, *dstatus;
+  FFCA_TRY(st.scratch(size_t(nb) * I * I * 16, &Q));
+  FFCA_TRY(st.scratch(size_t(nb) * 4, &dstatus));
+  FFCA_CK(cudaMemsetAsync(dstatus, 0, size_t(nb) * 4, s));
+  FFCA_TRY(launch_inv_PH(dtype, I, a.P, (double2*)Q, (int*)dstatus, nb, s));
+  a.Q = Q;
+  FFCA_TRY(launch_points(dtype, a, s));
+  FFCA_TRY(st.flush());
+  return finish_status((const int*)dstatus, status, nb, mem, s, FFCA_ST_SINGULAR_P);
+}

@@ -227,7 +227,7 @@ def run_fastfca(
 
 
 def run_fastfca_batch(y, P0, lam0, v0, iterations=20, inner_iterations=1, v_floor=None,
-                      record_likelihood=False, mem=None, stream=None):
+                      record_likelihood=False, stream=None, out=None):
     """Batched extension: U independent mixtures in one launch.
 
     y (U, I, N, F), P0 (U, F, I, I), lam0 (U, J, F, I), v0 (U, J, N, F);
@@ -247,7 +247,7 @@ def run_fastfca_batch(y, P0, lam0, v0, iterations=20, inner_iterations=1, v_floo
         mode, vfs, vfa = _lib.VF_SCALAR, float(v_floor), None
     else:
         mode, vfs, vfa = _lib.VF_BIN, 0.0, _as_r(np.reshape(v_floor, (U, F)), c64)
-    P, lam, v = np.empty_like(P0), np.empty_like(lam0), np.empty_like(v0)
+    P, lam, v = out if out is not None else (np.empty_like(P0), np.empty_like(lam0), np.empty_like(v0))
     ll = np.empty((U, 1 + 2 * iterations)) if record_likelihood else None
     rc = lib.ffca_fastfca_run(_lib.device(), stream, _lib.MEM_HOST, code, U, I, J, N, F,
                               _lib.ptr(y), _lib.ptr(P0), _lib.ptr(lam0), _lib.ptr(v0), mode, vfs,
@@ -255,3 +255,141 @@ def run_fastfca_batch(y, P0, lam0, v0, iterations=20, inner_iterations=1, v_floo
                               _lib.ptr(P), _lib.ptr(lam), _lib.ptr(v), _lib.ptr(ll), None, None)
     _lib.check(rc, "ffca_fastfca_run")
     return P, lam, v, ll
+
+
+# ---------------------------------------------------------------------------
+# unfused public steps (each one a device call)
+# ---------------------------------------------------------------------------
+
+
+def _code(c64):
+    return _lib.C64 if c64 else _lib.C128
+
+
+def transform_observations(P: np.ndarray, obs: ObservationTensor) -> np.ndarray:
+    """y_tilde(n,f) = P(f)^H y(n,f), returned as (N, F, I).  fastfca.py:113-116."""
+    lib = _lib.require_gpu()
+    c64 = obs.data.dtype == np.complex64
+    I, N, F = obs.data.shape
+    P = _as_c(P, c64)
+    if P.shape != (F, I, I):
+        raise DimensionMismatch(f"P must be (F, I, I) = {(F, I, I)}, got {P.shape}")
+    out = np.empty((N, F, I), obs.data.dtype)
+    _lib.check(lib.ffca_transform(_lib.device(), None, _lib.MEM_HOST, _code(c64), 1, I, N, F,
+                                  _lib.ptr(obs.data), _lib.ptr(P), _lib.ptr(out)), "ffca_transform")
+    return out
+
+
+def mixture_weights(params: FastFcaParams) -> np.ndarray:
+    """w_i(n,f) = max(sum_j v_j Lambda_j,ii, floor) as (N, F, I).  fastfca.py:138-141."""
+    lib = _lib.require_gpu()
+    c64 = params.P.dtype == np.complex64
+    J, N, F = params.v.shape
+    I = params.order
+    out = np.empty((N, F, I), np.float32 if c64 else np.float64)
+    _lib.check(lib.ffca_mixture_weights(_lib.device(), None, _lib.MEM_HOST, _code(c64), 1, I, J, N, F,
+                                        _lib.ptr(params.Lam), _lib.ptr(params.v), _lib.ptr(out)),
+               "ffca_mixture_weights")
+    return out
+
+
+def e_step_diag(params: FastFcaParams, y_t: np.ndarray) -> TransformedStats:
+    """mu_t = (a/w) y_t, phi_t = max(a - a^2/w, 0), entrywise.  fastfca.py:144-157."""
+    lib = _lib.require_gpu()
+    c64 = params.P.dtype == np.complex64
+    J, N, F = params.v.shape
+    I = params.order
+    yt = _as_c(y_t, c64)
+    if yt.shape != (N, F, I):
+        raise DimensionMismatch(f"y_t must be (N, F, I) = {(N, F, I)}, got {yt.shape}")
+    mu = np.empty((J, N, F, I), yt.dtype)
+    phi = np.empty((J, N, F, I), np.float32 if c64 else np.float64)
+    _lib.check(lib.ffca_fastfca_estep_yt(_lib.device(), None, _lib.MEM_HOST, _code(c64), 1, I, J, N, F,
+                                         _lib.ptr(yt), _lib.ptr(params.Lam), _lib.ptr(params.v),
+                                         _lib.ptr(mu), _lib.ptr(phi)), "ffca_fastfca_estep_yt")
+    return TransformedStats(mu=mu, phi=phi)
+
+
+def m_step_diag(stats: TransformedStats, params: FastFcaParams,
+                v_floor: float | np.ndarray = 0.0) -> FastFcaParams:
+    """v then Lambda from transformed statistics; P untouched.  fastfca.py:160-181."""
+    lib = _lib.require_gpu()
+    c64 = params.P.dtype == np.complex64
+    J, N, F = params.v.shape
+    I = params.order
+    mu, phi = _as_c(stats.mu, c64), _as_r(stats.phi, c64)
+    mode, vfs, vfa = _floor_args(v_floor, J, N, F, c64)
+    if mode == _lib.VF_AUTO:
+        raise ValueError("m_step_diag needs an explicit v_floor")
+    v_new = np.empty((J, N, F), np.float32 if c64 else np.float64)
+    lam_new = np.empty((J, F, I), v_new.dtype)
+    _lib.check(lib.ffca_mstep_diag(_lib.device(), None, _lib.MEM_HOST, _code(c64), 1, I, J, N, F,
+                                   _lib.ptr(mu), _lib.ptr(phi), _lib.ptr(params.Lam), mode, vfs, _lib.ptr(vfa),
+                                   _lib.ptr(v_new), _lib.ptr(lam_new)), "ffca_mstep_diag")
+    return FastFcaParams(P=params.P, Lam=lam_new, v=v_new)
+
+
+def fixed_point_update_P(params: FastFcaParams, obs: ObservationTensor, inner_iterations: int = 1,
+                         counters: OpCounters | None = None) -> np.ndarray:
+    """Column-wise fixed-point map, ``inner_iterations`` times.  fastfca.py:197-237."""
+    _check_obs(obs, params)
+    lib = _lib.require_gpu()
+    c64 = obs.data.dtype == np.complex64
+    J, N, F = params.v.shape
+    I = params.order
+    P = _as_c(params.P, c64)
+    out = np.empty_like(P)
+    _lib.check(lib.ffca_fixed_point_update_P(_lib.device(), None, _lib.MEM_HOST, _code(c64), 1, I, J, N, F,
+                                             _lib.ptr(obs.data), _lib.ptr(P), _lib.ptr(_as_r(params.Lam, c64)),
+                                             _lib.ptr(_as_r(params.v, c64)), int(inner_iterations),
+                                             _lib.ptr(out), None), "ffca_fixed_point_update_P")
+    if counters is not None:
+        counters.add_inversions((I + 1) * F * int(inner_iterations))
+    return out
+
+
+def log_likelihood(params: FastFcaParams, obs: ObservationTensor) -> float:
+    """Observed log likelihood in the transformed basis.  fastfca.py:240-255."""
+    _check_obs(obs, params)
+    lib = _lib.require_gpu()
+    c64 = obs.data.dtype == np.complex64
+    J, N, F = params.v.shape
+    I = params.order
+    ll = np.empty(1)
+    _lib.check(lib.ffca_fastfca_loglik(_lib.device(), None, _lib.MEM_HOST, _code(c64), 1, I, J, N, F,
+                                       _lib.ptr(obs.data), _lib.ptr(_as_c(params.P, c64)),
+                                       _lib.ptr(_as_r(params.Lam, c64)), _lib.ptr(_as_r(params.v, c64)),
+                                       _lib.ptr(ll), None), "ffca_fastfca_loglik")
+    if not np.isfinite(ll[0]):
+        raise SingularP("basis transform is singular")
+    return float(ll[0])
+
+
+def back_transform_means(P: np.ndarray, mu_t: np.ndarray, images_layout: bool = False) -> np.ndarray:
+    """Solve P^H mu = mu_tilde per bin; (J, N, F, I) in and out.  fastfca.py:258-273."""
+    lib = _lib.require_gpu()
+    c64 = np.asarray(mu_t).dtype == np.complex64
+    mu_t = _as_c(mu_t, c64)
+    P = _as_c(P, c64)
+    J, N, F, I = mu_t.shape
+    if P.shape != (F, I, I):
+        raise DimensionMismatch(f"P must be (F, I, I) = {(F, I, I)}, got {P.shape}")
+    out = np.empty((J, I, N, F) if images_layout else (J, N, F, I), mu_t.dtype)
+    _lib.check(lib.ffca_back_transform(_lib.device(), None, _lib.MEM_HOST, _code(c64), 1, I, J, N, F,
+                                       _lib.ptr(P), _lib.ptr(mu_t), _lib.ptr(out), 1 if images_layout else 0,
+                                       None), "ffca_back_transform")
+    return out
+
+
+def images_from_state(obs: ObservationTensor, params: FastFcaParams) -> np.ndarray:
+    """Fused stats refresh + Wiener back-solve: images (J, I, N, F) from the final state."""
+    lib = _lib.require_gpu()
+    c64 = obs.data.dtype == np.complex64
+    J, N, F = params.v.shape
+    I = params.order
+    out = np.empty((J, I, N, F), obs.data.dtype)
+    _lib.check(lib.ffca_fastfca_images(_lib.device(), None, _lib.MEM_HOST, _code(c64), 1, I, J, N, F,
+                                       _lib.ptr(obs.data), _lib.ptr(_as_c(params.P, c64)),
+                                       _lib.ptr(_as_r(params.Lam, c64)), _lib.ptr(_as_r(params.v, c64)),
+                                       _lib.ptr(out), None), "ffca_fastfca_images")
+    return out

@@ -94,3 +94,57 @@ def make(cfg: Config, seed0: int = 0, mixtures: int | None = None):
         yu, Pu, lu, vu, _ = mixture(seed0 + u, cfg.I, cfg.J, cfg.F, cfg.N, cfg.rank, cfg.zero_frac)
         y[u], P[u], lam[u], v[u] = yu, Pu, lu, vu
     return y, P, lam, v
+
+
+def make_torch(cfg: Config, seed: int, mixtures: int, device, chunk: int = 32):
+    """The same recipe drawn with torch on the GPU (fast for the 256-mixture config).
+
+    Used by bench.py only; the draws differ from ``make`` (different RNG) but
+    follow the identical distributions.  Returns device tensors in the
+    reference layouts with a leading mixture axis, cast to the config dtype.
+    """
+    import torch
+
+    I, J, F, N, r = cfg.I, cfg.J, cfg.F, cfg.N, cfg.rank
+    cdt = torch.complex64 if cfg.dtype == "c64" else torch.complex128
+    rdt = torch.float32 if cfg.dtype == "c64" else torch.float64
+    gen = torch.Generator(device=device)
+    gen.manual_seed(int(seed))
+    y = torch.empty((mixtures, I, N, F), dtype=cdt, device=device)
+    v0 = torch.empty((mixtures, J, N, F), dtype=rdt, device=device)
+    eye = torch.eye(I, dtype=torch.complex128, device=device)
+
+    def cn(shape):
+        re = torch.randn(shape, dtype=torch.float64, device=device, generator=gen)
+        im = torch.randn(shape, dtype=torch.float64, device=device, generator=gen)
+        return torch.complex(re, im) * SQRT_HALF
+
+    def gamma(shape):
+        # Gamma(shape 1/2, scale 1) is exactly Z^2 / 2 with Z ~ N(0, 1)
+        z = torch.randn(shape, dtype=torch.float64, device=device, generator=gen)
+        return 0.5 * z * z
+
+    for u0 in range(0, mixtures, chunk):
+        U = min(chunk, mixtures - u0)
+        A = cn((U, J, F, I, I))
+        R = A @ A.conj().transpose(-1, -2) + 0.01 * eye
+        L = torch.linalg.cholesky(R)
+        W = gamma((U, J, F, r))
+        H = gamma((U, J, r, N))
+        vt = (W @ H).transpose(-1, -2).contiguous()  # (U, J, N, F)
+        if cfg.zero_frac > 0:
+            mask = torch.rand((U, J, N, F), dtype=torch.float64, device=device, generator=gen) < cfg.zero_frac
+            vt = vt.masked_fill(mask, 0.0)
+        yy = torch.zeros((U, N, F, I), dtype=torch.complex128, device=device)
+        for j in range(J):
+            z = cn((U, N, F, I))
+            yy += torch.sqrt(vt[:, j])[..., None] * torch.einsum("ufab,unfb->unfa", L[:, j], z)
+        yi = yy.permute(0, 3, 1, 2).contiguous()  # (U, I, N, F)
+        y[u0:u0 + U] = yi.to(cdt)
+        power = (yi.real ** 2 + yi.imag ** 2).mean(dim=1)  # (U, N, F)
+        jit = 0.9 + 0.2 * torch.rand((U, J, N, F), dtype=torch.float64, device=device, generator=gen)
+        v0[u0:u0 + U] = ((power / J)[:, None] * jit).to(rdt)
+        del A, R, L, W, H, vt, yy, yi
+    P0 = torch.eye(I, dtype=cdt, device=device).expand(mixtures, F, I, I).contiguous()
+    lam0 = torch.ones((mixtures, J, F, I), dtype=rdt, device=device)
+    return y, P0, lam0, v0

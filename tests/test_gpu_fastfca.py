@@ -1,0 +1,322 @@
+"""GPU parity of the FastFCA-AS path against the CPU oracle and the reference golden vectors.
+
+Tolerances (BASELINE.json north_star):
+  per-iteration state check   rel <= 1e-10 (complex128), <= 1e-4 (complex64)
+  end to end                  log-likelihood rel <= 1e-6 (fp64); images rel-L2 <= 1e-3 (fp32)
+rel = max|a - b| / max|b| (test_fastfca.py:364-366) unless stated.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import rel
+from oracle import fastfca_ref as ffr
+from paper_1805_09498_b200 import ObservationTensor, _lib, errors, fastfca, wiener
+from paper_1805_09498_b200.workloads import CONFIGS, mixture
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["g33", "g44", "g86", "g22", "g12", "g23"]
+TOL = {"c128": 1e-10, "c64": 1e-4}
+
+
+def relL2(a, b):
+    return float(np.linalg.norm((np.asarray(a) - b).ravel()) / np.linalg.norm(np.asarray(b).ravel()))
+
+
+def case(golden, key):
+    return {k.split("/", 1)[1]: v for k, v in golden.items() if k.startswith(key + "/")}
+
+
+def cast(dt, *arrs):
+    out = []
+    for a in arrs:
+        if dt == "c64":
+            a = a.astype(np.complex64) if np.iscomplexobj(a) else a.astype(np.float32)
+        out.append(a)
+    return out
+
+
+@pytest.fixture(autouse=True)
+def _plan_env():
+    old = os.environ.pop("FFCA_FORCE_PLAN", None)
+    yield
+    os.environ.pop("FFCA_FORCE_PLAN", None)
+    if old is not None:
+        os.environ["FFCA_FORCE_PLAN"] = old
+
+
+# ---------------------------------------------------------------------------
+# against the unmodified reference (golden vectors)
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("dt", ["c128", "c64"])
+@pytest.mark.parametrize("key", CASES)
+def test_fused_loop_golden(golden, key, dt):
+    g = case(golden, key)
+    y, P0, lam0, v0 = cast(dt, g["y"], g["P0"], g["lam0"], g["v0"])
+    it = int(g["iters"])
+    run = fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=it,
+                              record_likelihood=True)
+    tol = TOL[dt] * (1 if dt == "c128" else 1)
+    assert rel(run.params.P, g["P"]) <= tol
+    assert rel(run.params.Lam, g["lam"]) <= tol
+    assert rel(run.params.v, g["v"]) <= tol
+    assert run.counters.inversions == int(g["inversions"]) and run.counters.matmuls == 0
+    ll = np.array([run.loglik_init] + run.loglik_after_em + run.loglik_after_p)
+    assert np.abs(ll - g["ll"]).max() <= (1e-12 if dt == "c128" else 1e-6) * np.abs(g["ll"]).max()
+    assert rel(run.stats.mu, g["mu"]) <= tol
+    assert rel(run.stats.phi, g["phi"]) <= tol
+    images = wiener.mmse_images_fastfca(run.params, run.stats).stft
+    assert rel(images, g["images"]) <= tol
+
+
+def test_inner_iterations_scalar_floor_golden(golden):
+    g = case(golden, "k2")
+    run = fastfca.run_fastfca(ObservationTensor(g["y"]), fastfca.FastFcaParams(g["P0"], g["lam0"], g["v0"]),
+                              iterations=3, inner_iterations=2, v_floor=0.0)
+    assert rel(run.params.P, g["P"]) <= 1e-10
+    assert rel(run.params.Lam, g["lam"]) <= 1e-10
+    assert rel(run.params.v, g["v"]) <= 1e-10
+    assert run.counters.inversions == int(g["inversions"])
+
+
+def test_unfused_steps_golden(golden):
+    g = case(golden, "step")
+    y, P, lam, v = g["y"], g["P"], g["lam"], g["v"]
+    obs = ObservationTensor(y)
+    params = fastfca.FastFcaParams(P, lam, v)
+    yt = fastfca.transform_observations(P, obs)
+    assert rel(yt, g["yt"]) <= 1e-13
+    assert rel(fastfca.mixture_weights(params), g["w"]) <= 1e-14
+    st = fastfca.e_step_diag(params, yt)
+    assert rel(st.mu, g["mu"]) <= 1e-12 and rel(st.phi, g["phi"]) <= 1e-12
+    em = fastfca.m_step_diag(st, params, v_floor=0.05)
+    assert rel(em.v, g["v_em"]) <= 1e-12 and rel(em.Lam, g["lam_em"]) <= 1e-12
+    Pn = fastfca.fixed_point_update_P(em, obs, inner_iterations=2)
+    assert rel(Pn, g["P_new"]) <= 1e-10
+    ll = fastfca.log_likelihood(params, obs)
+    assert abs(ll - float(g["ll"])) <= 1e-12 * abs(float(g["ll"]))
+    assert rel(fastfca.back_transform_means(P, st.mu), g["back"]) <= 1e-12
+    one = fastfca.run_fastfca(obs, params, iterations=1, v_floor=0.0)
+    assert rel(one.params.P, g["one_iter_P"]) <= 1e-10
+
+
+# ---------------------------------------------------------------------------
+# per-iteration state check (same state fed into one iteration)
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("dt", ["c128", "c64"])
+@pytest.mark.parametrize("shape", [(3, 3, 40, 200), (4, 4, 12, 300), (8, 6, 6, 160), (2, 3, 9, 77)])
+def test_one_iteration_from_state(dt, shape):
+    I, J, F, N = shape
+    y, P0, lam0, v0, _ = mixture(31 + I, I, J, F, N, 4, 0.0)
+    st = ffr.run_fastfca(y, P0, lam0, v0, iterations=3, stats=False)  # a non-trivial state
+    y_, P_, l_, v_ = cast(dt, y, st.P, st.lam, st.v)
+    # the oracle sees exactly the (possibly rounded) state the GPU sees
+    y64, P64, l64, v64 = (a.astype(np.complex128) if np.iscomplexobj(a) else a.astype(np.float64)
+                          for a in (y_, P_, l_, v_))
+    vf = ffr.power_floor(y64)
+    ref = ffr.run_fastfca(y64, P64, l64, v64, iterations=1, v_floor=vf, stats=False)
+    run = fastfca.run_fastfca(ObservationTensor(y_), fastfca.FastFcaParams(P_, l_, v_), iterations=1,
+                              v_floor=vf)
+    tol = TOL[dt]
+    assert rel(run.params.v, ref.v) <= tol
+    assert rel(run.params.Lam, ref.lam) <= tol
+    assert rel(run.params.P, ref.P) <= tol
+
+
+# ---------------------------------------------------------------------------
+# end to end at BASELINE config 0 (full size) and the complex64 path on it
+# ---------------------------------------------------------------------------
+
+
+@pytest.fixture(scope="module")
+def config0():
+    cfg = CONFIGS[0]
+    y, P0, lam0, v0, _ = mixture(0, cfg.I, cfg.J, cfg.F, cfg.N, cfg.rank)
+    ref = ffr.run_fastfca(y, P0, lam0, v0, iterations=cfg.iterations, record_likelihood=True)
+    return cfg, (y, P0, lam0, v0), ref
+
+
+def test_end_to_end_config0_fp64(config0):
+    cfg, (y, P0, lam0, v0), ref = config0
+    run = fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0),
+                              iterations=cfg.iterations, record_likelihood=True)
+    assert abs(run.loglik_after_p[-1] - ref.loglik_after_p[-1]) <= 1e-6 * abs(ref.loglik_after_p[-1])
+    lls = np.array(run.loglik_after_p)
+    assert np.abs(lls - ref.loglik_after_p).max() <= 1e-10 * abs(ref.loglik_after_p[-1])
+    assert rel(run.params.P, ref.P) <= 1e-10
+    assert rel(run.params.v, ref.v) <= 1e-10
+    images = wiener.mmse_images_fastfca(run.params, run.stats).stft
+    assert relL2(images, ffr.images(ref.P, ref.mu)) <= 1e-10
+
+
+def test_end_to_end_config0_fp32(config0):
+    cfg, (y, P0, lam0, v0), ref = config0
+    y32, P32, l32, v32 = cast("c64", y, P0, lam0, v0)
+    run = fastfca.run_fastfca(ObservationTensor(y32), fastfca.FastFcaParams(P32, l32, v32),
+                              iterations=cfg.iterations, record_likelihood=True)
+    images = wiener.mmse_images_fastfca(run.params, run.stats).stft
+    assert images.dtype == np.complex64
+    assert relL2(images, ffr.images(ref.P, ref.mu)) <= 1e-3
+    assert abs(run.loglik_after_p[-1] - ref.loglik_after_p[-1]) <= 1e-4 * abs(ref.loglik_after_p[-1])
+
+
+# ---------------------------------------------------------------------------
+# launch-plan coverage: clusters (DSMEM reduction) and the global-slab path
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("plan", ["1,2,1", "1,4,1", "1,8,1", "2,1,0", "1,4,0", "4,1,1", "1,1,1"])
+@pytest.mark.parametrize("dt", ["c128", "c64"])
+def test_forced_plans_agree(plan, dt):
+    y, P0, lam0, v0, _ = mixture(77, 3, 3, 11, 150, 4, 0.0)
+    y, P0, lam0, v0 = cast(dt, y, P0, lam0, v0)
+    base = fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=4,
+                               record_likelihood=True)
+    os.environ["FFCA_FORCE_PLAN"] = plan
+    run = fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=4,
+                              record_likelihood=True)
+    tol = 1e-12 if dt == "c128" else 1e-5
+    assert rel(run.params.P, base.params.P) <= tol
+    assert rel(run.params.v, base.params.v) <= tol
+    lltol = 1e-12 if dt == "c128" else 1e-6  # fp32 partial sums are grouped differently per plan
+    assert abs(run.loglik_after_p[-1] - base.loglik_after_p[-1]) <= lltol * abs(base.loglik_after_p[-1])
+
+
+def test_long_recording_slice_cluster_path():
+    # config-2 shape (I=J=4, N=9375, rank-8 NMF, complex64) on a few bins: the
+    # bin is longer than one CTA's shared memory, so a cluster splits the frames
+    cfg = CONFIGS[2]
+    F = 6
+    y, P0, lam0, v0, _ = mixture(2, cfg.I, cfg.J, F, cfg.N, cfg.rank)
+    ref = ffr.run_fastfca(y, P0, lam0, v0, iterations=5, stats=False)
+    out = (np.zeros(6, np.int32))
+    _lib.load().ffca_plan_loop(0, _lib.C64, 1, cfg.I, cfg.J, cfg.N, F, _lib.VF_AUTO,
+                               out.ctypes.data_as(_lib._ip))
+    assert out[1] > 1  # clustered
+    y32, P32, l32, v32 = cast("c64", y, P0, lam0, v0)
+    run = fastfca.run_fastfca(ObservationTensor(y32), fastfca.FastFcaParams(P32, l32, v32), iterations=5)
+    assert rel(run.params.P, ref.P) <= 1e-4
+    assert rel(run.params.Lam, ref.lam) <= 1e-4
+    assert rel(run.params.v, ref.v) <= 1e-4
+
+
+def test_large_array_slice_with_zero_cells():
+    # config-4 shape (I=8, J=6, N=4000, 10% zero cells) on a few bins
+    cfg = CONFIGS[4]
+    F = 4
+    y, P0, lam0, v0, _ = mixture(4, cfg.I, cfg.J, F, cfg.N, cfg.rank, cfg.zero_frac)
+    ref = ffr.run_fastfca(y, P0, lam0, v0, iterations=3, stats=False)
+    run64 = fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=3)
+    assert rel(run64.params.P, ref.P) <= 1e-10 and rel(run64.params.v, ref.v) <= 1e-10
+    y32, P32, l32, v32 = cast("c64", y, P0, lam0, v0)
+    run = fastfca.run_fastfca(ObservationTensor(y32), fastfca.FastFcaParams(P32, l32, v32), iterations=3)
+    assert np.isfinite(run.params.v).all() and np.isfinite(run.params.P).all()
+    assert rel(run.params.P, ref.P) <= 1e-4
+    assert rel(run.params.Lam, ref.lam) <= 1e-4
+    assert rel(run.params.v, ref.v) <= 1e-4
+
+
+# ---------------------------------------------------------------------------
+# batching, determinism, floors, edge cases, errors
+# ---------------------------------------------------------------------------
+
+
+def test_batch_equals_single_mixtures_bitwise():
+    ys, Ps, ls, vs = [], [], [], []
+    for s in range(3):
+        y, P0, lam0, v0, _ = mixture(100 + s, 3, 3, 13, 50)
+        ys.append(y), Ps.append(P0), ls.append(lam0), vs.append(v0)
+    Pb, lb, vb, llb = fastfca.run_fastfca_batch(np.stack(ys), np.stack(Ps), np.stack(ls), np.stack(vs),
+                                                iterations=4, record_likelihood=True)
+    for u in range(3):
+        run = fastfca.run_fastfca(ObservationTensor(ys[u]), fastfca.FastFcaParams(Ps[u], ls[u], vs[u]),
+                                  iterations=4, record_likelihood=True)
+        assert np.array_equal(run.params.P, Pb[u])
+        assert np.array_equal(run.params.v, vb[u])
+        assert run.loglik_after_p[-1] == llb[u, -1]
+
+
+def test_deterministic_bitwise():
+    y, P0, lam0, v0, _ = mixture(9, 4, 4, 17, 300, 8)
+    a = fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=6)
+    b = fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=6)
+    assert np.array_equal(a.params.P, b.params.P) and np.array_equal(a.params.v, b.params.v)
+
+
+@pytest.mark.parametrize("kind", ["bin", "full", "scalar"])
+def test_floor_modes(kind):
+    y, P0, lam0, v0, _ = mixture(3, 3, 2, 9, 60)
+    J, N, F = v0.shape
+    if kind == "bin":
+        vf = 0.3 * ffr.power_floor(y) * 1e9  # large enough to bind
+    elif kind == "full":
+        vf = np.random.default_rng(1).uniform(0.0, 0.2, (J, N, F)) * np.abs(y).mean() ** 2
+    else:
+        vf = 0.05
+    ref = ffr.run_fastfca(y, P0, lam0, v0, iterations=3, v_floor=vf, stats=False)
+    run = fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=3,
+                              v_floor=vf)
+    assert rel(run.params.v, ref.v) <= 1e-10 and rel(run.params.P, ref.P) <= 1e-10
+
+
+def test_zero_iterations_keeps_params():
+    y, P0, lam0, v0, _ = mixture(4, 2, 2, 3, 5)
+    run = fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=0,
+                              record_likelihood=True)
+    assert np.array_equal(run.params.P, P0) and np.array_equal(run.params.v, v0)
+    assert run.counters.inversions == 0
+    assert run.stats.mu.shape == (2, 5, 3, 2)
+    assert run.loglik_after_em == [] and run.loglik_after_p == []
+    assert abs(run.loglik_init - ffr.log_likelihood(P0, lam0, v0, y)) <= 1e-12 * abs(run.loglik_init)
+
+
+def test_single_frame_single_channel():
+    y, P0, lam0, v0, _ = mixture(6, 1, 2, 4, 1)
+    ref = ffr.run_fastfca(y, P0, lam0, v0, iterations=2, stats=False)
+    run = fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=2)
+    assert rel(run.params.P, ref.P) <= 1e-10 and rel(run.params.v, ref.v) <= 1e-10
+
+
+def test_singular_P_raises():
+    y, P0, lam0, v0, _ = mixture(8, 2, 2, 3, 10)
+    P0[1] = 0.0
+    with pytest.raises(errors.SingularP):
+        fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=1)
+
+
+def test_zero_bin_raises_singular_weighted_covariance():
+    y, P0, lam0, v0, _ = mixture(8, 2, 2, 3, 10)
+    y[:, :, 2] = 0.0  # B_i = 0 for that bin, stays singular after trace loading
+    with pytest.raises(errors.SingularWeightedCovariance):
+        fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=1)
+    with pytest.raises(ffr.OracleSingular):
+        ffr.run_fastfca(y, P0, lam0, v0, iterations=1)
+
+
+def test_channel_mismatch_raises():
+    y, P0, lam0, v0, _ = mixture(8, 3, 2, 3, 10)
+    with pytest.raises(errors.DimensionMismatch):
+        fastfca.run_fastfca(ObservationTensor(y[:2]), fastfca.FastFcaParams(P0, lam0, v0), iterations=1)
+
+
+def test_partition_identity_images():
+    # sum_j x_j = y (test_wiener.py:56-74; acceptance criterion 8)
+    y, P0, lam0, v0, _ = mixture(12, 3, 3, 16, 40)
+    run = fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=5)
+    fused = wiener.mmse_images_fastfca(run.params, run.stats).stft
+    assert np.abs(fused.sum(axis=0) - y).max() <= 1e-8 * np.abs(y).max()
+    explicit = wiener.mmse_images_fastfca(run.params, fastfca.TransformedStats(run.stats.mu, run.stats.phi)).stft
+    assert rel(fused, explicit) <= 1e-12
+
+
+def test_launch_count_is_one_kernel():
+    y, P0, lam0, v0, _ = mixture(12, 3, 3, 16, 40)
+    fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=20)
+    assert _lib.launches() == 1
