@@ -9,8 +9,8 @@
 namespace ffca {
 
 using LoopFn = void (*)(const LoopArgs);
-LoopFn loop_kernel_f32(int I, int J, bool res);
-LoopFn loop_kernel_f64(int I, int J, bool res);
+LoopFn loop_kernel_f32(int I, int J, int G, bool res);
+LoopFn loop_kernel_f64(int I, int J, int G, bool res);
 
 static bool hot_shape(int I, int J) {
   return (I == 3 && J == 3) || (I == 4 && J == 4) || (I == 8 && J == 6) || (I == 2 && J == 2);
@@ -34,7 +34,7 @@ struct LoopPlan {
 static constexpr size_t kSlabBudget = 96 * 1024;
 
 static int choose_threads(int G, int NL) {
-  const int per_bin = (NL + 7) / 8;  // ~8 frames per thread per pass
+  const int per_bin = (NL + 3) / 4;  // ~4 frames per thread per pass (capped at 256 threads)
   int t = G * per_bin;
   t = (t + 31) / 32 * 32;
   if (t < 64) t = 64;
@@ -47,7 +47,8 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
   const int rsz = int(rsize(dtype));
   const int JM = hot_shape(I, J) ? J : 8;
   const int VMAX = host_vmax(I, JM);
-  const int G0 = dtype == FFCA_C64 ? 4 : 2;
+  // lane-interleaved bin groups only for the exact-J instantiations
+  const int G0 = hot_shape(I, J) ? (dtype == FFCA_C64 ? 4 : 2) : 1;
   auto fill = [&](int G, int C, bool res) {
     p.G = G;
     p.C = C;
@@ -62,14 +63,20 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
   // Test hook: FFCA_FORCE_PLAN="G,C,resident" pins the launch plan (parity tests
   // use it to exercise the cluster and global-slab paths at small sizes).
   if (const char* fp = getenv("FFCA_FORCE_PLAN")) {
-    int G = 1, C = 1, res = 1;
-    if (sscanf(fp, "%d,%d,%d", &G, &C, &res) == 3 && (G == 1 || G == 2 || G == 4) && C >= 1 && C <= 8 &&
-        (C & (C - 1)) == 0 && C <= N && (C == 1 || G == 1)) {
+    int G = 1, C = 1, res = 1, thr = 0;
+    const int nf = sscanf(fp, "%d,%d,%d,%d", &G, &C, &res, &thr);
+    if (nf >= 3 && (G == 1 || G == G0) && (G == 1 || res) && C >= 1 && C <= 8 && (C & (C - 1)) == 0 && C <= N &&
+        (C == 1 || G == 1)) {
       fill(G, C, res != 0);
+      if (nf == 4 && thr >= 64 && thr <= 256 && thr % 32 == 0) {
+        p.threads = thr;
+        LoopSmem L(I, J, G, p.NL, thr / 32, rsz, vf_mode, res != 0, VMAX);
+        p.smem = L.total;
+      }
       if (p.smem <= smem_optin) return FFCA_OK;
     }
   }
-  for (int G = G0; G >= 1; G >>= 1) {
+  for (int G : {G0, 1}) {
     fill(G, 1, true);
     if (p.slab <= kSlabBudget && p.smem <= smem_optin) return FFCA_OK;
   }
@@ -78,7 +85,7 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
     fill(1, C, true);
     if (p.slab <= kSlabBudget && p.smem <= smem_optin) return FFCA_OK;
   }
-  fill(G0, 1, false);  // too long for the cluster: stream the slab from global scratch
+  fill(1, 1, false);  // too long for the cluster: stream the slab from global scratch
   if (p.smem > smem_optin) {
     set_error("problem too large: %zu B shared memory needed", p.smem);
     return FFCA_E_UNSUPPORTED;
@@ -181,8 +188,7 @@ static int loop_entry(int device, void* stream, int mem, int dtype, int U, int I
   a.scratch = scratch;
   a.slab_bytes = (long long)p.slab;
 
-  const bool res_tpl = p.resident && hot_shape(I, J);
-  LoopFn fn = dtype == FFCA_C64 ? loop_kernel_f32(I, J, res_tpl) : loop_kernel_f64(I, J, res_tpl);
+  LoopFn fn = dtype == FFCA_C64 ? loop_kernel_f32(I, J, p.G, p.resident) : loop_kernel_f64(I, J, p.G, p.resident);
   if (!fn) {
     set_error("no kernel for I=%d J=%d", I, J);
     return FFCA_E_UNSUPPORTED;

@@ -28,9 +28,22 @@ template <> struct Floors<float> {
   static constexpr float vmin = 1e-30f;
 };
 
-// IEEE reciprocal / quotient in the arithmetic type.
-__device__ __forceinline__ double rcp(double x) { return 1.0 / x; }
-__device__ __forceinline__ float rcp(float x) { return __frcp_rn(x); }
+// Reciprocals: hardware approximation refined by Newton steps (fp64: two
+// steps from MUFU.RCP64H give full double precision; fp32: one step).  The
+// operands here are floored positive weights / powers, never 0, inf or
+// subnormal, so the IEEE special-case paths of 1/x are not needed.
+__device__ __forceinline__ double rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = fma(r, fma(-x, r, 1.0), r);
+  r = fma(r, fma(-x, r, 1.0), r);
+  return r;
+}
+__device__ __forceinline__ float rcp(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return fmaf(r, fmaf(-x, r, 1.0f), r);
+}
 __device__ __forceinline__ double quot(double a, double b) { return a / b; }
 __device__ __forceinline__ float quot(float a, float b) { return __fdiv_rn(a, b); }
 __device__ __forceinline__ double flog(double x) { return log(x); }
@@ -70,11 +83,17 @@ __device__ __forceinline__ double2 cmul(const double2 a, const double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 __device__ __forceinline__ double2 crecip(const double2 z) {
-  // 1/z = conj(z)/|z|^2 with a scaling step against over/underflow
-  double s = fmax(fabs(z.x), fabs(z.y));
-  double zr = z.x / s, zi = z.y / s;
-  double d = zr * zr + zi * zi;
-  return make_double2(zr / (d * s), -zi / (d * s));
+  // 1/z = conj(z) / |z|^2; rescale by an exact power of two outside
+  // [2^-500, 2^500] so |z|^2 neither overflows nor underflows.
+  const double m = fmax(fabs(z.x), fabs(z.y));
+  if (m > 0x1p-500 && m < 0x1p500) {
+    const double r = 1.0 / (z.x * z.x + z.y * z.y);
+    return make_double2(z.x * r, -z.y * r);
+  }
+  const int e = ilogb(m);
+  const double zr = scalbn(z.x, -e), zi = scalbn(z.y, -e);
+  const double r = 1.0 / (zr * zr + zi * zi);
+  return make_double2(scalbn(zr * r, -e), scalbn(-zi * r, -e));
 }
 
 // In-place LU with partial pivoting of one I x I complex matrix stored
@@ -152,6 +171,158 @@ __device__ double lu_logabsdet(const double2* a) {
   for (int k = 0; k < I; ++k) s += log(hypot(a[k * I + k].x, a[k * I + k].y));
   return s;
 }
+
+// ------------------------------------------------------------------------
+// Register-resident small solvers (fully unrolled; static indexing only, so
+// the matrices stay in registers for I <= 4).  Used by the loop kernel's
+// per-bin P update:
+//   lu_p:   partial-pivoting LU of P (pivot |re|+|im|, LAPACK izamax), with the
+//           reciprocal pivots kept so the solves need no division.
+//   ldl_b:  LDL^H of the Hermitian weighted covariance B_i.
+// Both report an exactly zero pivot, which is when numpy.linalg.inv raises.
+// ------------------------------------------------------------------------
+template <int I>
+struct SmallLU {
+  double2 a[I][I];  // L (unit, strictly lower) and U
+  double2 rd[I];    // 1 / U_kk
+  int piv[I];
+  bool ok;
+  double logabsdet;
+
+  __device__ __forceinline__ void factor() {
+    ok = true;
+    logabsdet = 0.0;
+#pragma unroll
+    for (int k = 0; k < I; ++k) {
+      int p = k;
+      double best = cabs1(a[k][k]);
+#pragma unroll
+      for (int r = k + 1; r < I; ++r) {
+        const double m = cabs1(a[r][k]);
+        if (m > best) { best = m; p = r; }
+      }
+      piv[k] = p;
+#pragma unroll
+      for (int r = k + 1; r < I; ++r) {
+        const bool sw = (r == p);
+#pragma unroll
+        for (int c = 0; c < I; ++c) {
+          const double2 t = a[k][c];
+          a[k][c] = sw ? a[r][c] : t;
+          a[r][c] = sw ? t : a[r][c];
+        }
+      }
+      const double2 d = a[k][k];
+      if (d.x == 0.0 && d.y == 0.0) ok = false;
+      rd[k] = crecip(d);
+      logabsdet += log(hypot(d.x, d.y));
+#pragma unroll
+      for (int r = k + 1; r < I; ++r) {
+        const double2 l = cmul(a[r][k], rd[k]);
+        a[r][k] = l;
+#pragma unroll
+        for (int c = k + 1; c < I; ++c) {
+          const double2 u = a[k][c];
+          a[r][c].x -= l.x * u.x - l.y * u.y;
+          a[r][c].y -= l.x * u.y + l.y * u.x;
+        }
+      }
+    }
+  }
+
+  // z = row `row` of A^{-1}, i.e. the solution of A^T z = e_row.
+  // With S A = L U (S the row swaps): U^T w = e, L^T t = w, z = S^T t.
+  __device__ __forceinline__ void inverse_row(int row, double2 (&z)[I]) const {
+    double2 w[I];
+#pragma unroll
+    for (int r = 0; r < I; ++r) {
+      double2 acc = make_double2(r == row ? 1.0 : 0.0, 0.0);
+#pragma unroll
+      for (int c = 0; c < r; ++c) {  // (U^T)_{r,c} = U_{c,r}
+        const double2 u = a[c][r];
+        acc.x -= u.x * w[c].x - u.y * w[c].y;
+        acc.y -= u.x * w[c].y + u.y * w[c].x;
+      }
+      w[r] = cmul(acc, rd[r]);
+    }
+#pragma unroll
+    for (int r = I - 1; r >= 0; --r) {
+      double2 acc = w[r];
+#pragma unroll
+      for (int c = r + 1; c < I; ++c) {  // (L^T)_{r,c} = L_{c,r}
+        const double2 l = a[c][r];
+        acc.x -= l.x * z[c].x - l.y * z[c].y;
+        acc.y -= l.x * z[c].y + l.y * z[c].x;
+      }
+      z[r] = acc;
+    }
+    // undo the swaps in reverse order: z = S^T t
+#pragma unroll
+    for (int k = I - 1; k >= 0; --k) {
+#pragma unroll
+      for (int r = k + 1; r < I; ++r) {
+        const bool sw = (r == piv[k]);
+        const double2 t = z[k];
+        z[k] = sw ? z[r] : t;
+        z[r] = sw ? t : z[r];
+      }
+    }
+  }
+};
+
+template <int I>
+struct SmallLDL {
+  double2 l[I][I];  // strictly lower part used
+  double rd[I];     // 1 / d_k
+  bool ok;
+
+  // B given as its lower triangle (diag real).  B = L D L^H.
+  __device__ __forceinline__ void factor(double2 (&b)[I][I]) {
+    ok = true;
+    double d[I];
+#pragma unroll
+    for (int k = 0; k < I; ++k) {
+      double dk = b[k][k].x;
+#pragma unroll
+      for (int c = 0; c < k; ++c) dk -= (l[k][c].x * l[k][c].x + l[k][c].y * l[k][c].y) * d[c];
+      d[k] = dk;
+      if (dk == 0.0) ok = false;
+      rd[k] = 1.0 / dk;
+#pragma unroll
+      for (int r = k + 1; r < I; ++r) {
+        double2 acc = b[r][k];
+#pragma unroll
+        for (int c = 0; c < k; ++c) {  // acc -= l[r][c] d_c conj(l[k][c])
+          const double2 lr = l[r][c], lk = l[k][c];
+          acc.x -= (lr.x * lk.x + lr.y * lk.y) * d[c];
+          acc.y -= (lr.y * lk.x - lr.x * lk.y) * d[c];
+        }
+        l[r][k] = make_double2(acc.x * rd[k], acc.y * rd[k]);
+      }
+    }
+  }
+
+  __device__ __forceinline__ void solve(double2 (&x)[I]) const {
+#pragma unroll
+    for (int r = 1; r < I; ++r)
+#pragma unroll
+      for (int c = 0; c < r; ++c) {
+        const double2 lv = l[r][c];
+        x[r].x -= lv.x * x[c].x - lv.y * x[c].y;
+        x[r].y -= lv.x * x[c].y + lv.y * x[c].x;
+      }
+#pragma unroll
+    for (int r = 0; r < I; ++r) x[r] = make_double2(x[r].x * rd[r], x[r].y * rd[r]);
+#pragma unroll
+    for (int r = I - 1; r >= 0; --r)
+#pragma unroll
+      for (int c = r + 1; c < I; ++c) {  // (L^H)_{r,c} = conj(l[c][r])
+        const double2 lv = l[c][r];
+        x[r].x -= lv.x * x[c].x + lv.y * x[c].y;
+        x[r].y -= lv.x * x[c].y - lv.y * x[c].x;
+      }
+  }
+};
 
 // Status bits written per bin (mapped to the reference's exceptions on host).
 enum : int {

@@ -12,10 +12,15 @@
 //   phase B  weighted covariances B_i = sum_n y y^H / w_i  (fastfca.py:352-358)
 //   reduce
 //   solve    P^-1, B_i^-1 [P^-H]_i per bin, fp64          (fastfca.py:359-370)
-// separated only by __syncthreads / cluster barriers.  Bins of a group are
-// interleaved lane-wise (bin = lane % G) so the one-time gather from the
-// reference's (I, N, F) layout reads whole 32-byte sectors and the compute
-// loops read shared memory conflict-free.
+// separated only by __syncthreads / cluster barriers.
+//
+// Slab layout: one record per (frame n, bin g) at index n*G + g, holding the
+// I complex observations (padded to an odd count RS) or the J powers (odd
+// JS).  Lane l of a warp touches record (slot*G + g) = l + const, so record
+// strides are odd and every LDS is bank-conflict free; a thread walks its
+// frames with one pointer increment and immediate offsets.  Bins are
+// interleaved lane-wise (g = lane % G) so the one-time gather from the
+// reference's (I, N, F) layout reads whole 32-byte sectors.
 #pragma once
 
 #include "common.cuh"
@@ -29,7 +34,7 @@ struct LoopArgs {
   int C;         // cluster size (CTAs sharing one bin group, split over n)
   int NL;        // max frames held by one CTA (ceil(N / C))
   int iters, K;
-  int p_only;     // skip the EM sweep: fixed_point_update_P (fastfca.py:197-237)
+  int p_only;    // skip the EM sweep: fixed_point_update_P (fastfca.py:197-237)
   int vf_mode;   // 0 scalar, 1 per-bin (U,F), 2 full (U,J,N,F), 3 auto (power floor)
   double vf_scalar;
   const void* vf;      // real array for modes 1, 2
@@ -48,6 +53,7 @@ struct LoopArgs {
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+__host__ __device__ constexpr int odd_up(int x) { return (x & 1) ? x : x + 1; }
 
 template <int I>
 struct Shape {
@@ -56,6 +62,7 @@ struct Shape {
   static constexpr int NCH = (I + IC - 1) / IC;
   static constexpr int NB = IC * I * I;  // reals per chunk
   static constexpr bool PREG = I <= 4;   // keep P / lambda in registers
+  static constexpr int RS = odd_up(I);   // complex per slab record
 };
 
 template <int I, int JM>
@@ -71,8 +78,8 @@ struct LoopSmem {
                                int VMAX) {
     size_t o = 0;
     const size_t csz = 2 * size_t(rsz);
-    ybytes = align16(size_t(I) * NL * G * csz);
-    vbytes = align16(size_t(J) * NL * G * rsz);
+    ybytes = align16(size_t(NL) * G * odd_up(I) * csz);
+    vbytes = align16(size_t(NL) * G * odd_up(J) * rsz);
     const size_t fs = vf_mode == 2 ? vbytes : 0;
     slab = ybytes + vbytes + fs;
     if (resident) {
@@ -102,6 +109,14 @@ struct LoopSmem {
   }
 };
 
+// Sum over the lanes of one bin (lanes sharing lane % G).
+template <int G, typename T>
+__device__ __forceinline__ T bin_warp_sum(T x) {
+#pragma unroll
+  for (int o = 16; o >= G; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+  return x;
+}
+
 // ------------------------------------------------------------------------
 // Sum V per-thread values over all threads of one bin in the cluster.
 // Result lands in tot[g*VMAX + k] (fp64) and is visible after return.
@@ -109,23 +124,21 @@ struct LoopSmem {
 // rank order.  cpart is double-buffered (parity) so a fast CTA cannot
 // overwrite partials a slower CTA is still reading over DSMEM.
 // ------------------------------------------------------------------------
-template <typename R, int V>
-__device__ __forceinline__ void bin_reduce(const R (&vals)[V], int nv, double* wpart, double* cpart,
-                                           double* tot, int G, int C, int VMAX, int& parity) {
+template <typename R, int V, int G>
+__device__ __forceinline__ void bin_reduce(const R (&vals)[V], double* wpart, double* cpart, double* tot, int C,
+                                           int VMAX, int& parity) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, W = blockDim.x >> 5;
-  const int g = tid % G;
+  const int g = lane % G;
 #pragma unroll
   for (int k = 0; k < V; ++k) {
-    if (k < nv) {
-      R s = warp_sum_seg(vals[k], G);
-      if (lane < G) wpart[(warp * G + g) * VMAX + k] = double(s);
-    }
+    const R s = bin_warp_sum<G>(vals[k]);
+    if (lane < G) wpart[(warp * G + g) * VMAX + k] = double(s);
   }
   __syncthreads();
   double* cp = cpart + parity * G * VMAX;
   double* dst = (C > 1) ? cp : tot;
-  for (int t = tid; t < G * nv; t += blockDim.x) {
-    const int gg = t / nv, k = t % nv;
+  for (int t = tid; t < G * V; t += blockDim.x) {
+    const int gg = t / V, k = t % V;
     double s = 0.0;
     for (int w = 0; w < W; ++w) s += wpart[(w * G + gg) * VMAX + k];
     dst[gg * VMAX + k] = s;
@@ -133,8 +146,8 @@ __device__ __forceinline__ void bin_reduce(const R (&vals)[V], int nv, double* w
   if (C > 1) {
     cg::cluster_group cl = cg::this_cluster();
     cl.sync();
-    for (int t = tid; t < G * nv; t += blockDim.x) {
-      const int gg = t / nv, k = t % nv;
+    for (int t = tid; t < G * V; t += blockDim.x) {
+      const int gg = t / V, k = t % V;
       double s = 0.0;
       for (int r = 0; r < C; ++r) s += cl.map_shared_rank(cp, r)[gg * VMAX + k];
       tot[gg * VMAX + k] = s;
@@ -144,16 +157,197 @@ __device__ __forceinline__ void bin_reduce(const R (&vals)[V], int nv, double* w
   __syncthreads();
 }
 
-template <typename R, int I, int JT, bool RES>
-__global__ void __launch_bounds__(256) ffca_loop_kernel(const LoopArgs a) {
+// Per-point work of one thread over its frames of one bin (registers only).
+template <typename R, int I, int JM, int G>
+struct PointWork {
+  using C2 = typename Cpx<R>::T;
+  static constexpr int IC = Shape<I>::IC, NB = Shape<I>::NB, RS = Shape<I>::RS;
+  static constexpr bool PREG = Shape<I>::PREG;
+  static constexpr int VA = JM * (1 + I) + 1;
+
+  C2* ys;
+  R* vs;
+  const R* vfs;
+  const C2* Pc;
+  const R* lamc;
+  int g, J, JS, rec0, rstep, npts;
+  R wfl, invI;
+  C2 Pr[PREG ? I : 1][PREG ? I : 1];
+  R Lr[PREG ? JM : 1][PREG ? I : 1];
+
+  __device__ __forceinline__ void load_PL() {
+    if constexpr (PREG) {
+#pragma unroll
+      for (int x = 0; x < I; ++x)
+#pragma unroll
+        for (int y2 = 0; y2 < I; ++y2) Pr[x][y2] = Pc[(g * I + x) * I + y2];
+#pragma unroll
+      for (int j = 0; j < JM; ++j)
+#pragma unroll
+        for (int i = 0; i < I; ++i) Lr[j][i] = (j < J) ? lamc[(g * J + j) * I + i] : R(0);
+    }
+  }
+  __device__ __forceinline__ C2 P(int x, int y2) const {
+    if constexpr (PREG) return Pr[x][y2];
+    else return Pc[(g * I + x) * I + y2];
+  }
+  __device__ __forceinline__ R Lam(int j, int i) const {
+    if constexpr (PREG) return Lr[j][i];
+    else return lamc[(g * J + j) * I + i];
+  }
+  // y_t = P^H y ; q = |y_t|^2   (fastfca.py:442-446)
+  __device__ __forceinline__ void transform_q(const C2 (&yv)[I], R (&q)[I]) const {
+#pragma unroll
+    for (int b = 0; b < I; ++b) {
+      C2 acc = mk<C2, R>(R(0), R(0));
+#pragma unroll
+      for (int x = 0; x < I; ++x) cmac_conj(acc, P(x, b), yv[x]);
+      q[b] = acc.x * acc.x + acc.y * acc.y;
+    }
+  }
+  // w_i = max(sum_j v_j lambda_ji, floor)   (fastfca.py:324)
+  __device__ __forceinline__ void weights(const R (&vj)[JM], R (&w)[I]) const {
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      R s = R(0);
+#pragma unroll
+      for (int j = 0; j < JM; ++j)
+        if (j < J) s = fma(vj[j], Lam(j, i), s);
+      w[i] = fmax(s, wfl);
+    }
+  }
+  __device__ __forceinline__ void load_point(const C2* yp, const R* vp, C2 (&yv)[I], R (&vj)[JM]) const {
+#pragma unroll
+    for (int i = 0; i < I; ++i) yv[i] = yp[i];
+#pragma unroll
+    for (int j = 0; j < JM; ++j) vj[j] = (j < J) ? vp[j] : R(0);
+  }
+
+  // Phase A: fused E/M sweep over this thread's frames (fastfca.py:323-340).
+  template <bool REC, bool VF2>
+  __device__ __forceinline__ void phaseA(R (&acc)[VA], const R vfl_b) {
+    const C2* yp = ys + rec0 * RS;
+    R* vp = vs + rec0 * JS;
+    const R* fp = vfs + rec0 * JS;
+#pragma unroll 1
+    for (int k = 0; k < npts; ++k, yp += rstep * RS, vp += rstep * JS, fp += rstep * JS) {
+      C2 yv[I];
+      R vj[JM], q[I], w[I], iw[I], qiw2[I], d[I];
+      load_point(yp, vp, yv, vj);
+      transform_q(yv, q);
+      weights(vj, w);
+#pragma unroll
+      for (int i = 0; i < I; ++i) {
+        iw[i] = rcp(w[i]);
+        qiw2[i] = (q[i] * iw[i]) * iw[i];
+        d[i] = qiw2[i] - iw[i];
+      }
+      if constexpr (REC) {
+        R l = R(0);
+#pragma unroll
+        for (int i = 0; i < I; ++i) l += flog(w[i]) + q[i] * iw[i];
+        acc[VA - 1] += l;
+      }
+#pragma unroll
+      for (int j = 0; j < JM; ++j) {
+        if (j < J) {
+          R r1 = R(0), r2 = R(0);
+#pragma unroll
+          for (int i = 0; i < I; ++i) {
+            r1 = fma(iw[i], Lam(j, i), r1);
+            r2 = fma(qiw2[i], Lam(j, i), r2);
+          }
+          const R v = vj[j];
+          const R step = (((r1 - r2) * v) * v) * invI;
+          R fl = vfl_b;
+          if constexpr (VF2) fl = fp[j];
+          const R vn = fmax(v - step, fl);
+          const R ratio = v * rcp(vn);
+          acc[j] += ratio;
+          const R rv = ratio * v;
+#pragma unroll
+          for (int i = 0; i < I; ++i) acc[JM + j * I + i] = fma(rv, d[i], acc[JM + j * I + i]);
+          vp[j] = vn;
+        }
+      }
+    }
+  }
+
+  // Phase B: weighted covariances for i-chunk ch (fastfca.py:352-358); with REC
+  // also the likelihood at (P, v', lambda') (after-EM evaluation).
+  template <bool REC>
+  __device__ __forceinline__ void phaseB(R (&acc)[NB + 1], int ch) const {
+    const C2* yp = ys + rec0 * RS;
+    const R* vp = vs + rec0 * JS;
+#pragma unroll 1
+    for (int k = 0; k < npts; ++k, yp += rstep * RS, vp += rstep * JS) {
+      C2 yv[I];
+      R vj[JM], w[I];
+      load_point(yp, vp, yv, vj);
+      weights(vj, w);
+      if constexpr (REC) {
+        R q[I];
+        transform_q(yv, q);
+        R l = R(0);
+#pragma unroll
+        for (int i = 0; i < I; ++i) l += flog(w[i]) + q[i] * rcp(w[i]);
+        acc[NB] += l;
+      }
+      // lower-triangle outer product: per row x: diag, then (x, y<x) re, im
+      R O[I * I];
+      {
+        int kk = 0;
+#pragma unroll
+        for (int x = 0; x < I; ++x) {
+          O[kk++] = yv[x].x * yv[x].x + yv[x].y * yv[x].y;
+#pragma unroll
+          for (int y2 = 0; y2 < x; ++y2) {
+            O[kk++] = yv[x].x * yv[y2].x + yv[x].y * yv[y2].y;
+            O[kk++] = yv[x].y * yv[y2].x - yv[x].x * yv[y2].y;
+          }
+        }
+      }
+#pragma unroll
+      for (int ii = 0; ii < IC; ++ii) {
+        const int i = ch * IC + ii;
+        if (i < I) {
+          const R iwv = rcp(w[i]);
+#pragma unroll
+          for (int kk = 0; kk < I * I; ++kk) acc[ii * I * I + kk] = fma(O[kk], iwv, acc[ii * I * I + kk]);
+        }
+      }
+    }
+  }
+
+  // Likelihood partial sum_n,i ln w + q / w at the current state.
+  __device__ __forceinline__ void phaseL(R (&acc)[1]) const {
+    const C2* yp = ys + rec0 * RS;
+    const R* vp = vs + rec0 * JS;
+#pragma unroll 1
+    for (int k = 0; k < npts; ++k, yp += rstep * RS, vp += rstep * JS) {
+      C2 yv[I];
+      R vj[JM], q[I], w[I];
+      load_point(yp, vp, yv, vj);
+      transform_q(yv, q);
+      weights(vj, w);
+#pragma unroll
+      for (int i = 0; i < I; ++i) acc[0] += flog(w[i]) + q[i] * rcp(w[i]);
+    }
+  }
+};
+
+template <typename R, int I, int JT, int G, bool RES>
+__global__ void __launch_bounds__(256, 2) ffca_loop_kernel(const LoopArgs a) {
   using C2 = typename Cpx<R>::T;
   constexpr int JM = JT > 0 ? JT : 8;
   constexpr int IC = Shape<I>::IC, NCH = Shape<I>::NCH, NB = Shape<I>::NB;
   constexpr bool PREG = Shape<I>::PREG;
+  constexpr int RS = Shape<I>::RS;
   constexpr int VMAX = loop_vmax<I, JM>();
   constexpr int VA = JM * (1 + I) + 1;
   const int J = JT > 0 ? JT : a.J;
-  const int G = a.G, C = a.C;
+  const int JS = odd_up(J);
+  const int C = a.C;
   const int tid = threadIdx.x;
   const int g = tid % G;
   const int slot = tid / G, nslots = blockDim.x / G;
@@ -200,34 +394,35 @@ __global__ void __launch_bounds__(256) ffca_loop_kernel(const LoopArgs a) {
   const C2* __restrict__ yg = (const C2*)a.y;
   const R* __restrict__ vg = (const R*)a.v_in;
 
-  // ---------------- load: gather (I,N,F) -> slab [i][n][g] ----------------
-  // idx % G == tid % G == g because blockDim is a multiple of G.
+  // ---------------- load: gather (I,N,F) -> slab records ----------------
+  // element e = (i * NL + n) * G + g' with g' fastest: consecutive lanes read
+  // consecutive bins (one 32-byte sector); e % G == tid % G == g.
   R psum = R(0);
-  for (int idx = tid; idx < I * NL * G; idx += blockDim.x) {
-    const int rest = idx / G;
+  for (int e = tid; e < I * NL * G; e += blockDim.x) {
+    const int rest = e / G;
     const int n = rest % NL, i = rest / NL;
     C2 val = mk<C2, R>(R(0), R(0));
     if (active && n < NLr) {
       val = yg[((u * I + i) * (long long)N + n0 + n) * F + f];
       psum += val.x * val.x + val.y * val.y;
     }
-    ys[idx] = val;
+    ys[(n * G + g) * RS + i] = val;
   }
-  for (int idx = tid; idx < J * NL * G; idx += blockDim.x) {
-    const int rest = idx / G;
+  for (int e = tid; e < J * NL * G; e += blockDim.x) {
+    const int rest = e / G;
     const int n = rest % NL, j = rest / NL;
     R val = R(0);
     if (active && n < NLr) val = vg[((u * J + j) * (long long)N + n0 + n) * F + f];
-    vs[idx] = val;
+    vs[(n * G + g) * JS + j] = val;
   }
   if (a.vf_mode == 2) {
     const R* vfg = (const R*)a.vf;
-    for (int idx = tid; idx < J * NL * G; idx += blockDim.x) {
-      const int rest = idx / G;
+    for (int e = tid; e < J * NL * G; e += blockDim.x) {
+      const int rest = e / G;
       const int n = rest % NL, j = rest / NL;
       R val = R(0);
       if (active && n < NLr) val = vfg[((u * J + j) * (long long)N + n0 + n) * F + f];
-      vfs[idx] = val;
+      vfs[(n * G + g) * JS + j] = val;
     }
   }
   for (int t = tid; t < G * I * I; t += blockDim.x) {
@@ -257,7 +452,7 @@ __global__ void __launch_bounds__(256) ffca_loop_kernel(const LoopArgs a) {
   // ---------------- v floor per bin (fca.py:82-89 when auto) ----------------
   if (a.vf_mode == 3) {
     const R pv[1] = {psum};
-    bin_reduce<R, 1>(pv, 1, wpart, cpart, tot, G, C, VMAX, parity);
+    bin_reduce<R, 1, G>(pv, wpart, cpart, tot, C, VMAX, parity);
     if (tid < G) {
       const double mean = tot[tid * VMAX] / (double(I) * double(N));
       const double fl = fmax(1e-10 * mean, double(Floors<R>::vmin));
@@ -274,178 +469,165 @@ __global__ void __launch_bounds__(256) ffca_loop_kernel(const LoopArgs a) {
   __syncthreads();
 
   const bool rec = a.ll != nullptr;
+  const bool vf2 = a.vf_mode == 2;
   const int nev = 1 + 2 * a.iters;
   const R wfl = Floors<R>::weight;
-  const R rI = R(I);
+  const R invI = R(1) / R(I);
   const double invN = 1.0 / double(N);
+  const int rec0 = slot * G + g;          // first record of this thread
+  const int rstep = nslots * G;           // records between a thread's frames (= blockDim.x)
+  const int npts = active ? (NLr > slot ? (NLr - slot + nslots - 1) / nslots : 0) : 0;
 
-  C2 Pr[PREG ? I : 1][PREG ? I : 1];
-  R Lr[PREG ? JM : 1][PREG ? I : 1];
-#define FFCA_LOAD_PL()                                                            \
-  if constexpr (PREG) {                                                           \
-    _Pragma("unroll") for (int x_ = 0; x_ < I; ++x_)                              \
-    _Pragma("unroll") for (int y_ = 0; y_ < I; ++y_) Pr[x_][y_] = Pc[(g * I + x_) * I + y_]; \
-    _Pragma("unroll") for (int j_ = 0; j_ < JM; ++j_)                             \
-    _Pragma("unroll") for (int i_ = 0; i_ < I; ++i_)                              \
-      Lr[j_][i_] = (j_ < J) ? lamc[(g * J + j_) * I + i_] : R(0);                  \
-  }
-#define FFCA_P(x_, y_) (PREG ? Pr[PREG ? (x_) : 0][PREG ? (y_) : 0] : Pc[(g * I + (x_)) * I + (y_)])
-#define FFCA_L(j_, i_) (PREG ? Lr[PREG ? (j_) : 0][PREG ? (i_) : 0] : lamc[(g * J + (j_)) * I + (i_)])
-  // y_t = P^H y ; q = |y_t|^2   (fastfca.py:442-446)
-#define FFCA_TRANSFORM_Q(yv_, q_)                                                 \
-  _Pragma("unroll") for (int b_ = 0; b_ < I; ++b_) {                              \
-    C2 acc_ = mk<C2, R>(R(0), R(0));                                              \
-    _Pragma("unroll") for (int a_ = 0; a_ < I; ++a_) cmac_conj(acc_, FFCA_P(a_, b_), yv_[a_]); \
-    q_[b_] = acc_.x * acc_.x + acc_.y * acc_.y;                                   \
-  }
-  // w_i = max(sum_j v_j lambda_ji, floor)   (fastfca.py:324)
-#define FFCA_WEIGHTS(vj_, w_)                                                     \
-  _Pragma("unroll") for (int i_ = 0; i_ < I; ++i_) {                              \
-    R s_ = R(0);                                                                  \
-    _Pragma("unroll") for (int j_ = 0; j_ < JM; ++j_) if (j_ < J) s_ = fma(vj_[j_], FFCA_L(j_, i_), s_); \
-    w_[i_] = fmax(s_, wfl);                                                       \
-  }
-#define FFCA_LOAD_POINT(n_, yv_, vj_)                                             \
-  _Pragma("unroll") for (int i_ = 0; i_ < I; ++i_) yv_[i_] = ys[(i_ * NL + (n_)) * G + g]; \
-  _Pragma("unroll") for (int j_ = 0; j_ < JM; ++j_) vj_[j_] = (j_ < J) ? vs[(j_ * NL + (n_)) * G + g] : R(0);
+  PointWork<R, I, JM, G> pw;
+  pw.ys = ys; pw.vs = vs; pw.vfs = vfs; pw.Pc = Pc; pw.lamc = lamc;
+  pw.g = g; pw.J = J; pw.JS = JS; pw.rec0 = rec0; pw.rstep = rstep; pw.npts = npts;
+  pw.wfl = wfl; pw.invI = invI;
 
   // ======================= outer iterations =======================
   for (int it = 0; it < a.iters; ++it) {
     // ---------------- phase A: fused E/M sweep ----------------
-    FFCA_LOAD_PL();
     double llA = 0.0;
     if (!a.p_only) {
+      pw.load_PL();
       R acc[VA];
 #pragma unroll
       for (int k = 0; k < VA; ++k) acc[k] = R(0);
       const R vfl_b = R(vfl[g]);
-      if (active) {
-        for (int n = slot; n < NLr; n += nslots) {
-          C2 yv[I];
-          R vj[JM], q[I], w[I], iw[I], qiw2[I];
-          FFCA_LOAD_POINT(n, yv, vj);
-          FFCA_TRANSFORM_Q(yv, q);
-          FFCA_WEIGHTS(vj, w);
+      if (rec) {
+        if (vf2) pw.template phaseA<true, true>(acc, vfl_b);
+        else pw.template phaseA<true, false>(acc, vfl_b);
+      } else {
+        if (vf2) pw.template phaseA<false, true>(acc, vfl_b);
+        else pw.template phaseA<false, false>(acc, vfl_b);
+      }
+      bin_reduce<R, VA, G>(acc, wpart, cpart, tot, C, VMAX, parity);
+      if (rec && tid < G) llA = tot[tid * VMAX + VA - 1];
+      // ---------------- lambda' per (bin, source) (fastfca.py:341-345) -------
+      for (int t = tid; t < G * J; t += blockDim.x) {
+        const int gg = t / J, j = t % J;
+        const double* T = tot + gg * VMAX;
+        const double s0 = T[j] * invN;
+        double mx = -1.0;
+        double ln[I];
 #pragma unroll
-          for (int i = 0; i < I; ++i) {
-            iw[i] = rcp(w[i]);
-            qiw2[i] = (q[i] * iw[i]) * iw[i];
-          }
-          if (rec) {
-            R l = R(0);
+        for (int i = 0; i < I; ++i) {
+          const double l = lamd[(gg * J + j) * I + i];
+          ln[i] = l * s0 + l * l * (T[JM + j * I + i] * invN);
+          mx = fmax(mx, ln[i]);
+        }
 #pragma unroll
-            for (int i = 0; i < I; ++i) l += flog(w[i]) + q[i] * iw[i];
-            acc[VA - 1] += l;
-          }
-#pragma unroll
-          for (int j = 0; j < JM; ++j) {
-            if (j < J) {
-              R r1 = R(0), r2 = R(0);
-#pragma unroll
-              for (int i = 0; i < I; ++i) {
-                r1 = fma(iw[i], FFCA_L(j, i), r1);
-                r2 = fma(qiw2[i], FFCA_L(j, i), r2);
-              }
-              const R v = vj[j];
-              const R step = quot(((r1 - r2) * v) * v, rI);
-              const R fl = (a.vf_mode == 2) ? vfs[(j * NL + n) * G + g] : vfl_b;
-              const R vn = fmax(v - step, fl);
-              const R ratio = quot(v, vn);
-              acc[j] += ratio;
-              const R rv = ratio * v;
-#pragma unroll
-              for (int i = 0; i < I; ++i) acc[JM + j * I + i] = fma(rv, qiw2[i] - iw[i], acc[JM + j * I + i]);
-              vs[(j * NL + n) * G + g] = vn;
-            }
-          }
+        for (int i = 0; i < I; ++i) {
+          const double x = fmax(ln[i], 1e-12 * mx);
+          lamd[(gg * J + j) * I + i] = x;
+          lamc[(gg * J + j) * I + i] = R(x);
         }
       }
-      bin_reduce<R, VA>(acc, rec ? VA : VA - 1, wpart, cpart, tot, G, C, VMAX, parity);
-      if (rec && tid < G) llA = tot[tid * VMAX + VA - 1];
+      __syncthreads();
     }
-    // ---------------- lambda' per (bin, source) ----------------
-    for (int t = tid; t < (a.p_only ? 0 : G * J); t += blockDim.x) {
-      const int gg = t / J, j = t % J;
-      const double* T = tot + gg * VMAX;
-      const double s0 = T[j] * invN;
-      double mx = -1.0;
-      double ln[I];
-#pragma unroll
-      for (int i = 0; i < I; ++i) {
-        const double l = lamd[(gg * J + j) * I + i];
-        ln[i] = l * s0 + l * l * (T[JM + j * I + i] * invN);
-        mx = fmax(mx, ln[i]);
-      }
-#pragma unroll
-      for (int i = 0; i < I; ++i) {
-        const double x = fmax(ln[i], 1e-12 * mx);
-        lamd[(gg * J + j) * I + i] = x;
-        lamc[(gg * J + j) * I + i] = R(x);
-      }
-    }
-    __syncthreads();
 
     // ---------------- phase B: weighted covariances ----------------
-    FFCA_LOAD_PL();
+    pw.load_PL();
     double llB = 0.0;
 #pragma unroll 1
     for (int ch = 0; ch < NCH; ++ch) {
       R acc[NB + 1];
 #pragma unroll
       for (int k = 0; k < NB + 1; ++k) acc[k] = R(0);
-      const bool rl = rec && ch == 0;
-      if (active) {
-        for (int n = slot; n < NLr; n += nslots) {
-          C2 yv[I];
-          R vj[JM], w[I];
-          FFCA_LOAD_POINT(n, yv, vj);
-          FFCA_WEIGHTS(vj, w);
-          if (rl) {
-            R q[I];
-            FFCA_TRANSFORM_Q(yv, q);
-            R l = R(0);
-#pragma unroll
-            for (int i = 0; i < I; ++i) l += flog(w[i]) + q[i] * rcp(w[i]);
-            acc[NB] += l;
-          }
-          // lower-triangle outer product: per row x: diag, then (x, y<x) re, im
-          R O[I * I];
-          {
-            int k = 0;
-#pragma unroll
-            for (int x = 0; x < I; ++x) {
-              O[k++] = yv[x].x * yv[x].x + yv[x].y * yv[x].y;
-#pragma unroll
-              for (int y2 = 0; y2 < x; ++y2) {
-                O[k++] = yv[x].x * yv[y2].x + yv[x].y * yv[y2].y;
-                O[k++] = yv[x].y * yv[y2].x - yv[x].x * yv[y2].y;
-              }
-            }
-          }
-#pragma unroll
-          for (int ii = 0; ii < IC; ++ii) {
-            const int i = ch * IC + ii;
-            if (i < I) {
-              const R iwv = rcp(w[i]);
-#pragma unroll
-              for (int k = 0; k < I * I; ++k) acc[ii * I * I + k] = fma(O[k], iwv, acc[ii * I * I + k]);
-            }
-          }
-        }
-      }
-      bin_reduce<R, NB + 1>(acc, rl ? NB + 1 : NB, wpart, cpart, tot, G, C, VMAX, parity);
-      if (rl && tid < G) llB = tot[tid * VMAX + NB];
+      if (rec && ch == 0) pw.template phaseB<true>(acc, ch);
+      else pw.template phaseB<false>(acc, ch);
+      bin_reduce<R, NB + 1, G>(acc, wpart, cpart, tot, C, VMAX, parity);
+      if (rec && ch == 0 && tid < G) llB = tot[tid * VMAX + NB];
       // keep this chunk of B in fp64 for the solve
       const int nbc = (ch == NCH - 1) ? (I - ch * IC) * I * I : NB;
       for (int t = tid; t < G * nbc; t += blockDim.x) {
-        const int gg = t / nbc, k = t % nbc;
-        bst[gg * I * I * I + ch * NB + k] = tot[gg * VMAX + k];
+        const int gg = t / nbc, kk = t % nbc;
+        bst[gg * I * I * I + ch * NB + kk] = tot[gg * VMAX + kk];
       }
     }
     __syncthreads();
 
     // ---------------- solve: P^-1 and new columns (fastfca.py:359-370) --------
-    {
+    if constexpr (I <= 4) {
+      // Thread (bin gg, s): s == 0 factors P (LU, partial pivoting) and
+      // publishes the factors; s = 1 + i factors B_i = L D L^H in registers.
+      // After one barrier every s >= 1 thread forms [P^-H]_i = conj(row i of
+      // P^-1) from the shared LU and solves B_i x = [P^-H]_i itself.
+      const int s = tid % (I + 1);
+      const int gg = tid / (I + 1);
+      const long long b = group * G + gg;
+      const bool bact = gg < G && b < a.total_bins;
+      double2* Ms = Msys + gg * (I + 1) * I * I;  // LU(P) + reciprocal pivots
+      int* pv = pivs + gg * (I + 1) * I;
+      SmallLDL<I> ldl;
+      if (bact && s > 0) {
+        const int i = s - 1;
+        const double* T = bst + gg * I * I * I + i * I * I;
+        double2 B[I][I];
+        double tr = 0.0;
+        int kk = 0;
+#pragma unroll
+        for (int x = 0; x < I; ++x) {
+          B[x][x] = make_double2(T[kk++] * invN, 0.0);
+          tr += B[x][x].x;
+#pragma unroll
+          for (int y2 = 0; y2 < x; ++y2) {
+            B[x][y2] = make_double2(T[kk] * invN, T[kk + 1] * invN);
+            kk += 2;
+          }
+        }
+        ldl.factor(B);
+        if (!ldl.ok) {  // one trace-loaded retry (fastfca.py:184-194)
+#pragma unroll
+          for (int x = 0; x < I; ++x) B[x][x].x += 1e-10 * tr;
+          ldl.factor(B);
+          if (crank == 0) atomicOr(&a.status[b], ldl.ok ? ST_B_LOADED : ST_SINGULAR_B);
+        }
+      }
+#pragma unroll 1
+      for (int k = 0; k < a.K; ++k) {
+        if (bact && s == 0) {
+          SmallLU<I> lu;
+#pragma unroll
+          for (int x = 0; x < I; ++x)
+#pragma unroll
+            for (int y2 = 0; y2 < I; ++y2) lu.a[x][y2] = Pd[(gg * I + x) * I + y2];
+          lu.factor();
+          if (!lu.ok && crank == 0) atomicOr(&a.status[b], ST_SINGULAR_P);
+          if (k == 0) ldet[gg] = lu.logabsdet;
+#pragma unroll
+          for (int x = 0; x < I; ++x) {
+#pragma unroll
+            for (int y2 = 0; y2 < I; ++y2) Ms[x * I + y2] = lu.a[x][y2];
+            Ms[I * I + x] = lu.rd[x];
+            pv[x] = lu.piv[x];
+          }
+        }
+        __syncthreads();
+        if (bact && s > 0) {
+          const int i = s - 1;
+          SmallLU<I> lu;
+#pragma unroll
+          for (int x = 0; x < I; ++x) {
+#pragma unroll
+            for (int y2 = 0; y2 < I; ++y2) lu.a[x][y2] = Ms[x * I + y2];
+            lu.rd[x] = Ms[I * I + x];
+            lu.piv[x] = pv[x];
+          }
+          double2 z[I];
+          lu.inverse_row(i, z);
+#pragma unroll
+          for (int x = 0; x < I; ++x) z[x].y = -z[x].y;  // [P^-H]_{x,i} = conj(P^-1_{i,x})
+          ldl.solve(z);
+#pragma unroll
+          for (int x = 0; x < I; ++x) {
+            Pd[(gg * I + x) * I + i] = z[x];
+            Pc[(gg * I + x) * I + i] = mk<C2, R>(R(z[x].x), R(z[x].y));
+          }
+        }
+        __syncthreads();
+      }
+    } else {
+      // I > 4: one thread per system on shared-memory matrices.
       const int s = tid % (I + 1);
       const int gg = tid / (I + 1);
       const long long b = group * G + gg;
@@ -458,21 +640,19 @@ __global__ void __launch_bounds__(256) ffca_loop_kernel(const LoopArgs a) {
         const double* T = bst + gg * I * I * I + i * I * I;
         double tr = 0.0;
         for (int pass = 0; pass < 2; ++pass) {
-          // full Hermitian B_i from the packed lower triangle, / N
-          int k = 0;
+          int kk = 0;
           for (int x = 0; x < I; ++x) {
-            const double d = T[k++] * invN;
-            Ms[x * I + x] = make_double2(d + (pass ? 1e-10 * tr : 0.0), 0.0);
-            if (!pass) tr += d;
+            const double dd = T[kk++] * invN;
+            Ms[x * I + x] = make_double2(dd + (pass ? 1e-10 * tr : 0.0), 0.0);
+            if (!pass) tr += dd;
             for (int y2 = 0; y2 < x; ++y2) {
-              const double re = T[k++] * invN, im = T[k++] * invN;
+              const double re = T[kk++] * invN, im = T[kk++] * invN;
               Ms[x * I + y2] = make_double2(re, im);
               Ms[y2 * I + x] = make_double2(re, -im);
             }
           }
           const bool okB = lu_factor<I>(Ms, pv);
           if (okB && pass == 0) break;
-          // one trace-loaded retry (fastfca.py:184-194)
           if (pass == 1 && crank == 0) atomicOr(&a.status[b], okB ? ST_B_LOADED : ST_SINGULAR_B);
         }
       }
@@ -517,20 +697,10 @@ __global__ void __launch_bounds__(256) ffca_loop_kernel(const LoopArgs a) {
 
   // ---------------- final likelihood evaluation (after the last P update) ----
   if (rec) {
-    FFCA_LOAD_PL();
+    pw.load_PL();
     R acc[1] = {R(0)};
-    if (active) {
-      for (int n = slot; n < NLr; n += nslots) {
-        C2 yv[I];
-        R vj[JM], q[I], w[I];
-        FFCA_LOAD_POINT(n, yv, vj);
-        FFCA_TRANSFORM_Q(yv, q);
-        FFCA_WEIGHTS(vj, w);
-#pragma unroll
-        for (int i = 0; i < I; ++i) acc[0] += flog(w[i]) + q[i] * rcp(w[i]);
-      }
-    }
-    bin_reduce<R, 1>(acc, 1, wpart, cpart, tot, G, C, VMAX, parity);
+    pw.phaseL(acc);
+    bin_reduce<R, 1, G>(acc, wpart, cpart, tot, C, VMAX, parity);
     if (tid < G) {
       const long long b = group * G + tid;
       double2* Ms = Msys + (tid * (I + 1)) * I * I;
@@ -541,19 +711,13 @@ __global__ void __launch_bounds__(256) ffca_loop_kernel(const LoopArgs a) {
         a.ll[b * nev + 2 * a.iters] = -tot[tid * VMAX] + 2.0 * double(N) * lu_logabsdet<I>(Ms);
     }
   }
-#undef FFCA_LOAD_PL
-#undef FFCA_P
-#undef FFCA_L
-#undef FFCA_TRANSFORM_Q
-#undef FFCA_WEIGHTS
-#undef FFCA_LOAD_POINT
 
   // ---------------- write back ----------------
   R* vo = (R*)a.v_out;
-  for (int idx = tid; idx < J * NL * G; idx += blockDim.x) {
-    const int rest = idx / G;
+  for (int e = tid; e < J * NL * G; e += blockDim.x) {
+    const int rest = e / G;
     const int n = rest % NL, j = rest / NL;
-    if (active && n < NLr) vo[((u * J + j) * (long long)N + n0 + n) * F + f] = vs[idx];
+    if (active && n < NLr) vo[((u * J + j) * (long long)N + n0 + n) * F + f] = vs[(n * G + g) * JS + j];
   }
   if (crank == 0) {
     for (int t = tid; t < G * I * I; t += blockDim.x) {

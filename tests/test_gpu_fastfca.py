@@ -172,7 +172,7 @@ def test_end_to_end_config0_fp32(config0):
 # ---------------------------------------------------------------------------
 
 
-@pytest.mark.parametrize("plan", ["1,2,1", "1,4,1", "1,8,1", "2,1,0", "1,4,0", "4,1,1", "1,1,1"])
+@pytest.mark.parametrize("plan", ["1,2,1", "1,4,1", "1,8,1", "1,1,0", "1,4,0", "4,1,1", "2,1,1", "1,1,1", "1,1,1,64"])
 @pytest.mark.parametrize("dt", ["c128", "c64"])
 def test_forced_plans_agree(plan, dt):
     y, P0, lam0, v0, _ = mixture(77, 3, 3, 11, 150, 4, 0.0)
