@@ -171,6 +171,15 @@ int ffca_mstep_diag(int device, void* stream, int mem, int dtype, int U, int I, 
                     const void* mu, const void* phi, const void* lam, int vf_mode, double vf_scalar,
                     const void* vf, void* v_out, void* lam_out);
 
+/* fca.m_step (fca.py:161-184) from mu (U,J,N,F,I), phi (U,J,N,F,I,I) and the old S. */
+int ffca_fca_mstep(int device, void* stream, int mem, int dtype, int U, int I, int J, int N, int F,
+                   const void* mu, const void* phi, const void* S, int vf_mode, double vf_scalar, const void* vf,
+                   void* S_out, void* v_out, int* status);
+
+/* fca.power_floor (fca.py:82-89): (U, F) float64. */
+int ffca_power_floor(int device, void* stream, int mem, int dtype, int U, int I, int N, int F, const void* y,
+                     double* out);
+
 /* Launch plan of the loop kernel for a shape: out6 = {G, C, NL, threads, resident, smem}. */
 int ffca_plan_loop(int device, int dtype, int U, int I, int J, int N, int F, int vf_mode, int* out6);
 

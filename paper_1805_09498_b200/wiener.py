@@ -9,7 +9,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import fastfca
+from . import fastfca, fca
+from .stft import ObservationTensor
 
 
 @dataclass
@@ -22,6 +23,14 @@ class SeparatedImages:
     @property
     def sources(self) -> int:
         return self.stft.shape[0]
+
+
+def mmse_images_fca(params: fca.FcaParams, obs: ObservationTensor) -> SeparatedImages:
+    """Wiener estimates from full-matrix parameters (a final E-step's means).  wiener.py:32-35.
+
+    The device writes the means directly in the (J, I, N, F) image layout.
+    """
+    return SeparatedImages(stft=fca.e_step(params, obs, images_layout=True).mu)
 
 
 def mmse_images_fastfca(params: fastfca.FastFcaParams, stats: fastfca.TransformedStats) -> SeparatedImages:

@@ -1,0 +1,86 @@
+"""The C-ABI library loads on a CPU-only host and exports every symbol include/ffca.h declares.
+
+No compute calls: there is no GPU here.  (gpu-marked tests exercise them.)
+"""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "ffca.h")
+LIB = os.path.join(ROOT, "paper_1805_09498_b200", "libffca_b200.so")
+
+
+def declared():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^(?:int|void|float|const char\*)\s+(ffca_\w+)\s*\(", text, re.M)))
+
+
+def test_header_declares_the_entry_points():
+    names = declared()
+    for must in ("ffca_fastfca_run", "ffca_fastfca_stats", "ffca_fastfca_images", "ffca_back_transform",
+                 "ffca_fastfca_loglik", "ffca_fixed_point_update_P", "ffca_fca_run", "ffca_fca_estep",
+                 "ffca_fca_loglik", "ffca_fca_mstep", "ffca_mstep_diag", "ffca_power_floor"):
+        assert must in names
+
+
+@pytest.mark.skipif(not os.path.exists(LIB), reason="library not built (run __graft_entry__.build())")
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(LIB)
+    missing = [n for n in declared() if not hasattr(lib, n)]
+    assert not missing, f"declared in ffca.h but not exported: {missing}"
+
+
+@pytest.mark.skipif(not os.path.exists(LIB), reason="library not built")
+def test_binding_table_matches_header():
+    from paper_1805_09498_b200 import _lib
+    assert set(_lib.SIGNATURES) == set(declared())
+    lib = _lib.load()
+    assert lib.ffca_version() >= 100
+    # no device in this container: the query must say so instead of crashing
+    assert lib.ffca_device_count() >= 0
+
+
+@pytest.mark.skipif(not os.path.exists(LIB), reason="library not built")
+def test_plan_introspection_without_device():
+    import numpy as np
+
+    from paper_1805_09498_b200 import _lib
+    lib = _lib.load()
+    out = np.zeros(6, np.int32)
+    # config 3 shape (c64, I=J=3, N=626): 4 lane-interleaved bins per CTA, resident
+    assert lib.ffca_plan_loop(0, _lib.C64, 256, 3, 3, 626, 513, _lib.VF_AUTO, out.ctypes.data_as(_lib._ip)) == 0
+    assert out[0] == 4 and out[1] == 1 and out[4] == 1
+    # config 2 shape (c64, I=J=4, N=9375): a cluster splits the frames
+    assert lib.ffca_plan_loop(0, _lib.C64, 1, 4, 4, 9375, 1025, _lib.VF_AUTO, out.ctypes.data_as(_lib._ip)) == 0
+    assert out[1] > 1 and out[4] == 1
+    # config 0 shape (c128): 2 bins per CTA
+    assert lib.ffca_plan_loop(0, _lib.C128, 1, 3, 3, 626, 513, _lib.VF_AUTO, out.ctypes.data_as(_lib._ip)) == 0
+    assert out[0] == 2
+
+
+def test_product_has_no_cpu_fallback(monkeypatch):
+    """Without a device the product path must fail loudly, never compute on the CPU."""
+    import numpy as np
+
+    from paper_1805_09498_b200 import _lib, errors, fastfca
+    from paper_1805_09498_b200.stft import ObservationTensor
+    if os.path.exists(LIB) and _lib.load().ffca_device_count() > 0:
+        pytest.skip("a GPU is visible")
+    obs = ObservationTensor(np.ones((2, 3, 4), complex))
+    params = fastfca.FastFcaParams(np.broadcast_to(np.eye(2), (4, 2, 2)), np.ones((1, 4, 2)), np.ones((1, 3, 4)))
+    with pytest.raises(errors.BackendUnavailable):
+        fastfca.run_fastfca(obs, params, iterations=1)
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_1805_09498_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith(".py"):
+                src = open(os.path.join(dirpath, fn)).read()
+                assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", src, re.M), fn

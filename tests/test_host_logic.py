@@ -1,0 +1,80 @@
+"""Host-side logic of the drop-in boundary (CPU only): layouts, dtype policy, argument mapping."""
+
+import numpy as np
+import pytest
+
+from paper_1805_09498_b200 import _lib, errors, fastfca, fca
+from paper_1805_09498_b200.evalkit import OpCounters, expected_counts
+from paper_1805_09498_b200.stft import ObservationTensor
+from paper_1805_09498_b200.workloads import CONFIGS, mixture
+
+
+def test_observation_dtype_policy():
+    z = np.ones((2, 3, 4), np.complex64)
+    assert ObservationTensor(z).data.dtype == np.complex64  # kept (documented extension)
+    assert ObservationTensor(z.astype(np.complex128)).data.dtype == np.complex128
+    assert ObservationTensor(np.ones((2, 3, 4))).data.dtype == np.complex128  # coerced as stft.py:63
+    with pytest.raises(errors.DimensionMismatch):
+        ObservationTensor(np.ones((2, 3)))
+    bad = np.ones((2, 3, 4), complex)
+    bad[0, 0, 0] = np.nan
+    with pytest.raises(ValueError):
+        ObservationTensor(bad)
+
+
+def test_params_validation_matches_reference_errors():
+    P = np.broadcast_to(np.eye(3), (5, 3, 3))
+    with pytest.raises(errors.DimensionMismatch):
+        fastfca.FastFcaParams(P, np.ones((2, 4, 3)), np.ones((2, 6, 5)))
+    with pytest.raises(errors.DimensionMismatch):
+        fastfca.FastFcaParams(P, np.ones((2, 5, 3)), np.ones((3, 6, 5)))
+    with pytest.raises(errors.DimensionMismatch):
+        fastfca.FastFcaParams(P, np.ones((2, 5, 3)), np.ones((2, 6, 4)))
+    p = fastfca.FastFcaParams(P, np.ones((2, 5, 3)), np.ones((2, 6, 5)))
+    assert p.P.dtype == np.complex128 and p.Lam.dtype == np.float64
+    assert (p.sources, p.bins, p.order) == (2, 5, 3)
+    p32 = fastfca.FastFcaParams(P.astype(np.complex64), np.ones((2, 5, 3)), np.ones((2, 6, 5)))
+    assert p32.Lam.dtype == np.float32 and p32.v.dtype == np.float32
+    with pytest.raises(errors.DimensionMismatch):
+        fca.FcaParams(np.ones((2, 5, 3, 2)), np.ones((2, 6, 5)))
+
+
+def test_v_floor_argument_mapping():
+    J, N, F = 2, 6, 5
+    assert fastfca._floor_args(None, J, N, F, False)[0] == _lib.VF_AUTO
+    m, s, a = fastfca._floor_args(0.25, J, N, F, False)
+    assert m == _lib.VF_SCALAR and s == 0.25 and a is None
+    m, _, a = fastfca._floor_args(np.arange(F, dtype=float), J, N, F, True)
+    assert m == _lib.VF_BIN and a.dtype == np.float32 and a.shape == (F,)
+    m, _, a = fastfca._floor_args(np.ones((J, 1, F)), J, N, F, False)
+    assert m == _lib.VF_FULL and a.shape == (J, N, F)
+
+
+def test_expected_counts_paper_values():
+    # PAPER.md:195-199,386-393 at I=J=3, N=249, F=512
+    assert expected_counts("fca", 3, 3, 249, 512).inversions == 129024
+    assert expected_counts("fca", 3, 3, 249, 512).matmuls == 764928
+    assert expected_counts("fastfca", 3, 3, 249, 512, 1).inversions == 2048
+    c = OpCounters()
+    c.add_inversions(3)
+    c.merge(OpCounters(2, 5))
+    assert c.as_dict() == {"inversions": 5, "matmuls": 5}
+    with pytest.raises(ValueError):
+        expected_counts("nope", 1, 1, 1, 1)
+
+
+def test_generator_shapes_and_determinism():
+    y, P0, lam0, v0, vt = mixture(3, 3, 2, 7, 11, 4, 0.1)
+    assert y.shape == (3, 11, 7) and P0.shape == (7, 3, 3) and lam0.shape == (2, 7, 3) and v0.shape == (2, 11, 7)
+    y2 = mixture(3, 3, 2, 7, 11, 4, 0.1)[0]
+    assert np.array_equal(y, y2)
+    assert (vt == 0).any()  # sparse-activity cells present
+    assert np.allclose(P0, np.eye(3)) and (lam0 == 1).all()
+    assert CONFIGS[3].point_iterations == 256 * 626 * 513 * 20
+
+
+def test_channel_mismatch_raises_before_any_device_call():
+    obs = ObservationTensor(np.ones((2, 3, 4), complex))
+    params = fastfca.FastFcaParams(np.broadcast_to(np.eye(3), (4, 3, 3)), np.ones((1, 4, 3)), np.ones((1, 3, 4)))
+    with pytest.raises(errors.DimensionMismatch):
+        fastfca.run_fastfca(obs, params, iterations=1)
