@@ -17,6 +17,21 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 void count_launch(int n) { g_launches += n; }
+
+void retain_pool(int dev) {
+  static std::mutex mu;
+  static bool done[64] = {false};
+  if (dev < 0 || dev >= 64) return;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaGetLastError();
+  done[dev] = true;
+}
 void reset_launches() { g_launches = 0; }
 bool timing_enabled() { return g_timing != 0; }
 void set_kernel_ms(float ms) { g_kernel_ms = ms; }

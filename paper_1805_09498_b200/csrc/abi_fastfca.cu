@@ -2,6 +2,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
+#include <vector>
 
 #include "ffca_loop.cuh"
 #include "host_common.h"
@@ -118,6 +120,229 @@ static int launch_loop(LoopFn fn, const LoopPlan& p, const LoopArgs& a, cudaStre
 
 using namespace ffca;
 
+// One (sub)problem with all arrays already on the device: plan, launch, optional timing.
+struct DevProblem {
+  int dtype, U, I, J, N, F;
+  int vf_mode;
+  double vf_scalar;
+  int iters, K, p_only;
+  const void *y, *P0, *lam0, *v0, *vf;
+  void *P, *lam, *v;
+  double* vf_out;
+  double* ll_bins;  // (U*F, nev) or null
+  int* status;      // (U*F)
+};
+
+static int launch_problem(int device, const DevProblem& d, cudaStream_t s) {
+  const long long nb = (long long)d.U * d.F;
+  if (nb == 0) return FFCA_OK;
+  int optin = 0;
+  FFCA_CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  LoopPlan p;
+  FFCA_TRY(plan_loop(d.dtype, d.I, d.J, d.N, nb, d.vf_mode, p, size_t(optin)));
+  void* scratch = nullptr;
+  if (!p.resident) FFCA_CK(cudaMallocAsync(&scratch, size_t(p.grid) * p.slab, s));
+  LoopArgs a;
+  a.U = d.U; a.I = d.I; a.J = d.J; a.N = d.N; a.F = d.F;
+  a.total_bins = nb;
+  a.G = p.G; a.C = p.C; a.NL = p.NL;
+  a.iters = d.iters; a.K = d.K; a.p_only = d.p_only;
+  a.vf_mode = d.vf_mode; a.vf_scalar = d.vf_scalar; a.vf = d.vf;
+  a.y = d.y; a.P_in = d.P0; a.lam_in = d.lam0; a.v_in = d.v0;
+  a.P_out = d.P; a.lam_out = d.lam; a.v_out = d.v;
+  a.vf_out = d.vf_out;
+  a.ll = d.ll_bins;
+  a.status = d.status;
+  a.scratch = scratch;
+  a.slab_bytes = (long long)p.slab;
+  LoopFn fn = d.dtype == FFCA_C64 ? loop_kernel_f32(d.I, d.J, p.G, p.resident)
+                                  : loop_kernel_f64(d.I, d.J, p.G, p.resident);
+  if (!fn) {
+    set_error("no kernel for I=%d J=%d", d.I, d.J);
+    return FFCA_E_UNSUPPORTED;
+  }
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (timing_enabled()) {
+    FFCA_CK(cudaEventCreate(&ev0));
+    FFCA_CK(cudaEventCreate(&ev1));
+    FFCA_CK(cudaEventRecord(ev0, s));
+  }
+  FFCA_TRY(launch_loop(fn, p, a, s));
+  FFCA_CK(cudaGetLastError());
+  if (ev0) {
+    FFCA_CK(cudaEventRecord(ev1, s));
+    FFCA_CK(cudaEventSynchronize(ev1));
+    float ms = 0.f;
+    FFCA_CK(cudaEventElapsedTime(&ms, ev0, ev1));
+    set_kernel_ms(ms);
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+  }
+  if (scratch) FFCA_CK(cudaFreeAsync(scratch, s));
+  return FFCA_OK;
+}
+
+// Array of layout (U, A, F, B) (elements of `es` bytes): the block of mixtures
+// [u0, u0+Uc) x bins [f0, f0+Fc) is Uc*A rows of Fc*B*es bytes at pitch F*B*es.
+struct Blk {
+  size_t A, B, es;
+};
+
+static int copy_blk(void* dst, const void* src, const Blk& b, int U, int F, int u0, int Uc, int f0, int Fc,
+                    bool h2d, cudaStream_t s) {
+  if (!dst || !src) return FFCA_OK;
+  const size_t pitch_full = size_t(F) * b.B * b.es, width = size_t(Fc) * b.B * b.es;
+  const size_t off = ((size_t(u0) * b.A) * F + f0) * b.B * b.es;
+  if (width == pitch_full) {  // whole rows: one linear copy
+    const size_t n = width * size_t(Uc) * b.A;
+    if (h2d)
+      FFCA_CK(cudaMemcpyAsync(dst, (const char*)src + off, n, cudaMemcpyHostToDevice, s));
+    else
+      FFCA_CK(cudaMemcpyAsync((char*)dst + off, src, n, cudaMemcpyDeviceToHost, s));
+    return FFCA_OK;
+  }
+  if (h2d)
+    FFCA_CK(cudaMemcpy2DAsync(dst, width, (const char*)src + off, pitch_full, width, size_t(Uc) * b.A,
+                              cudaMemcpyHostToDevice, s));
+  else
+    FFCA_CK(cudaMemcpy2DAsync((char*)dst + off, pitch_full, src, width, width, size_t(Uc) * b.A,
+                              cudaMemcpyDeviceToHost, s));
+  (void)U;
+  return FFCA_OK;
+}
+
+// Host-mode call split into chunks so that H2D of chunk c+1, the kernel of
+// chunk c and the D2H of chunk c-1 overlap (three internal streams, two
+// device buffer sets).  Chunks are mixture blocks (U > 1) or frequency
+// blocks of a single mixture; bins are independent, so the results are
+// bitwise those of one launch.
+static int pipelined_host_run(int device, cudaStream_t user, const DevProblem& proto, bool rec, int nchunk,
+                              bool by_mixture,
+                              const void* y, const void* P0, const void* lam0, const void* v0, const void* vf,
+                              void* P_out, void* lam_out, void* v_out, double* ll_out, double* vf_out,
+                              int* status_out) {
+  const int U = proto.U, I = proto.I, J = proto.J, N = proto.N, F = proto.F;
+  const size_t rs = rsize(proto.dtype), cs = csize(proto.dtype);
+  const long long nb = (long long)U * F;
+  const int nev = 1 + 2 * proto.iters;
+  const Blk By{size_t(I) * N, 1, cs}, BP{1, size_t(I) * I, cs}, Bl{size_t(J), size_t(I), rs},
+      Bv{size_t(J) * N, 1, rs}, Bvb{1, 1, rs}, Bvo{1, 1, 8}, Bst{1, 1, 4}, Bll{1, size_t(nev), 8};
+  const int cu = by_mixture ? (U + nchunk - 1) / nchunk : 1;
+  const int cf = by_mixture ? F : (F + nchunk - 1) / nchunk;
+  auto bytes = [&](const Blk& b) { return size_t(cu) * b.A * cf * b.B * b.es; };
+
+  cudaStream_t sin, scomp, sout;
+  FFCA_CK(cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking));
+  FFCA_CK(cudaStreamCreateWithFlags(&scomp, cudaStreamNonBlocking));
+  FFCA_CK(cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking));
+  cudaEvent_t start;
+  FFCA_CK(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  FFCA_CK(cudaEventRecord(start, user));  // order after prior work on the caller's stream
+  FFCA_CK(cudaStreamWaitEvent(sin, start, 0));
+  cudaEvent_t ev_in[2], ev_k[2], ev_out[2];
+  for (int k = 0; k < 2; ++k) {
+    FFCA_CK(cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming));
+    FFCA_CK(cudaEventCreateWithFlags(&ev_k[k], cudaEventDisableTiming));
+    FFCA_CK(cudaEventCreateWithFlags(&ev_out[k], cudaEventDisableTiming));
+  }
+  // device buffers: two slots of chunk inputs/outputs + full status / ll
+  std::vector<void*> allocs;
+  auto dalloc = [&](size_t n, void** p) -> int {
+    *p = nullptr;
+    if (n == 0) return FFCA_OK;
+    FFCA_CK(cudaMallocAsync(p, n, sin));
+    allocs.push_back(*p);
+    return FFCA_OK;
+  };
+  void *dy[2], *dP0[2], *dl0[2], *dv0[2], *dvf[2] = {nullptr, nullptr}, *dP[2], *dl[2], *dv[2], *dvo[2] = {nullptr, nullptr},
+       *dst[2], *dll[2] = {nullptr, nullptr};
+  int rc = FFCA_OK;
+  for (int k = 0; k < 2 && rc == FFCA_OK; ++k) {
+    rc = dalloc(bytes(By), &dy[k]);
+    if (!rc) rc = dalloc(bytes(BP), &dP0[k]);
+    if (!rc) rc = dalloc(bytes(Bl), &dl0[k]);
+    if (!rc) rc = dalloc(bytes(Bv), &dv0[k]);
+    if (!rc && proto.vf_mode == 1) rc = dalloc(bytes(Bvb), &dvf[k]);
+    if (!rc && proto.vf_mode == 2) rc = dalloc(bytes(Bv), &dvf[k]);
+    if (!rc) rc = dalloc(bytes(BP), &dP[k]);
+    if (!rc) rc = dalloc(bytes(Bl), &dl[k]);
+    if (!rc) rc = dalloc(bytes(Bv), &dv[k]);
+    if (!rc && vf_out) rc = dalloc(bytes(Bvo), &dvo[k]);
+    if (!rc) rc = dalloc(bytes(Bst), &dst[k]);
+    if (!rc && rec) rc = dalloc(bytes(Bll), &dll[k]);
+  }
+  void *fstatus = nullptr, *fll = nullptr, *llmix = nullptr;
+  if (!rc) rc = dalloc(size_t(nb) * 4, &fstatus);
+  if (!rc && rec) rc = dalloc(size_t(nb) * nev * 8, &fll);
+  if (!rc && rec && ll_out) rc = dalloc(size_t(U) * nev * 8, &llmix);
+  int nch = 0;
+  for (int c0 = 0; !rc && c0 < (by_mixture ? U : F); c0 += (by_mixture ? cu : cf), ++nch) {
+    const int k = nch & 1;
+    const int u0 = by_mixture ? c0 : 0, Uc = by_mixture ? std::min(cu, U - c0) : 1;
+    const int f0 = by_mixture ? 0 : c0, Fc = by_mixture ? F : std::min(cf, F - c0);
+    // slot k free again once chunk nch-2's kernel consumed its inputs / D2H drained its outputs
+    if (nch >= 2) {
+      rc = cudaStreamWaitEvent(sin, ev_k[k], 0) == cudaSuccess ? FFCA_OK : FFCA_E_CUDA;
+      if (!rc) rc = cudaStreamWaitEvent(scomp, ev_out[k], 0) == cudaSuccess ? FFCA_OK : FFCA_E_CUDA;
+    }
+    if (!rc) rc = copy_blk(dy[k], y, By, U, F, u0, Uc, f0, Fc, true, sin);
+    if (!rc) rc = copy_blk(dP0[k], P0, BP, U, F, u0, Uc, f0, Fc, true, sin);
+    if (!rc) rc = copy_blk(dl0[k], lam0, Bl, U, F, u0, Uc, f0, Fc, true, sin);
+    if (!rc) rc = copy_blk(dv0[k], v0, Bv, U, F, u0, Uc, f0, Fc, true, sin);
+    if (!rc && proto.vf_mode == 1) rc = copy_blk(dvf[k], vf, Bvb, U, F, u0, Uc, f0, Fc, true, sin);
+    if (!rc && proto.vf_mode == 2) rc = copy_blk(dvf[k], vf, Bv, U, F, u0, Uc, f0, Fc, true, sin);
+    if (rc) break;
+    FFCA_CK(cudaEventRecord(ev_in[k], sin));
+    FFCA_CK(cudaStreamWaitEvent(scomp, ev_in[k], 0));
+    FFCA_CK(cudaMemsetAsync(dst[k], 0, size_t(Uc) * Fc * 4, scomp));
+    DevProblem d = proto;
+    d.U = Uc;
+    d.F = Fc;
+    d.y = dy[k]; d.P0 = dP0[k]; d.lam0 = dl0[k]; d.v0 = dv0[k]; d.vf = dvf[k];
+    d.P = dP[k]; d.lam = dl[k]; d.v = dv[k]; d.vf_out = (double*)dvo[k];
+    d.ll_bins = (double*)dll[k];
+    d.status = (int*)dst[k];
+    rc = launch_problem(device, d, scomp);
+    if (rc) break;
+    // scatter the per-bin status / likelihood parts into the full-size buffers
+    FFCA_CK(cudaMemcpy2DAsync((char*)fstatus + (size_t(u0) * F + f0) * 4, size_t(F) * 4, dst[k], size_t(Fc) * 4,
+                              size_t(Fc) * 4, size_t(Uc), cudaMemcpyDeviceToDevice, scomp));
+    if (rec)
+      FFCA_CK(cudaMemcpy2DAsync((char*)fll + (size_t(u0) * F + f0) * nev * 8, size_t(F) * nev * 8, dll[k],
+                                size_t(Fc) * nev * 8, size_t(Fc) * nev * 8, size_t(Uc), cudaMemcpyDeviceToDevice,
+                                scomp));
+    FFCA_CK(cudaEventRecord(ev_k[k], scomp));
+    FFCA_CK(cudaStreamWaitEvent(sout, ev_k[k], 0));
+    rc = copy_blk(P_out, dP[k], BP, U, F, u0, Uc, f0, Fc, false, sout);
+    if (!rc) rc = copy_blk(lam_out, dl[k], Bl, U, F, u0, Uc, f0, Fc, false, sout);
+    if (!rc) rc = copy_blk(v_out, dv[k], Bv, U, F, u0, Uc, f0, Fc, false, sout);
+    if (!rc && vf_out) rc = copy_blk(vf_out, dvo[k], Bvo, U, F, u0, Uc, f0, Fc, false, sout);
+    if (!rc) FFCA_CK(cudaEventRecord(ev_out[k], sout));
+  }
+  if (!rc) {
+    FFCA_CK(cudaStreamSynchronize(scomp));
+    if (rec && ll_out) {
+      rc = reduce_ll((const double*)fll, (double*)llmix, U, F, nev, -double(N) * F * I * std::log(M_PI), scomp);
+      if (!rc) FFCA_CK(cudaMemcpyAsync(ll_out, llmix, size_t(U) * nev * 8, cudaMemcpyDeviceToHost, scomp));
+    }
+    FFCA_CK(cudaStreamSynchronize(sout));
+    if (!rc) rc = finish_status((const int*)fstatus, status_out, nb, FFCA_MEM_HOST, scomp,
+                                FFCA_ST_SINGULAR_P | FFCA_ST_SINGULAR_B);
+  }
+  for (void* q : allocs) cudaFreeAsync(q, scomp);
+  cudaStreamSynchronize(scomp);
+  for (int k = 0; k < 2; ++k) {
+    cudaEventDestroy(ev_in[k]);
+    cudaEventDestroy(ev_k[k]);
+    cudaEventDestroy(ev_out[k]);
+  }
+  cudaEventDestroy(start);
+  cudaStreamDestroy(sin);
+  cudaStreamDestroy(scomp);
+  cudaStreamDestroy(sout);
+  return rc;
+}
+
 static int loop_entry(int device, void* stream, int mem, int dtype, int U, int I, int J, int N, int F,
                       const void* y, const void* P0, const void* lam0, const void* v0, int vf_mode,
                       double vf_scalar, const void* vf, int iterations, int inner_iterations,
@@ -148,14 +373,33 @@ static int loop_entry(int device, void* stream, int mem, int dtype, int U, int I
   const int nev = 1 + 2 * iterations;
   if (nb == 0) return FFCA_OK;
 
+  DevProblem d = {};
+  d.dtype = dtype; d.U = U; d.I = I; d.J = J; d.N = N; d.F = F;
+  d.vf_mode = vf_mode; d.vf_scalar = vf_scalar;
+  d.iters = iterations; d.K = inner_iterations; d.p_only = p_only;
+
+  // host mode with a large input: pipeline H2D / compute / D2H over chunks
+  const size_t in_bytes = size_t(U) * I * N * F * cs + size_t(U) * J * N * F * rs;
+  // FFCA_NO_PIPELINE=1 disables, FFCA_PIPELINE_MIN_BYTES overrides the threshold (tests)
+  const char* nopipe = getenv("FFCA_NO_PIPELINE");
+  const char* minb = getenv("FFCA_PIPELINE_MIN_BYTES");
+  const size_t threshold = minb ? size_t(atoll(minb)) : (size_t(64) << 20);
+  if (mem == FFCA_MEM_HOST && in_bytes >= threshold && !(nopipe && nopipe[0] == '1')) {
+    const bool by_mix = U >= 2;
+    const int nchunk = by_mix ? std::min(U, 8) : std::min(F, 8);
+    if (nchunk >= 2) {
+      return pipelined_host_run(device, s, d, record_likelihood != 0, nchunk, by_mix, y, P0, lam0, v0, vf, P_out, lam_out, v_out,
+                                record_likelihood ? ll_out : nullptr, vf_out, status);
+    }
+  }
+
   Staging st(mem, s);
-  const void *dy, *dP, *dl, *dv, *dvf = nullptr;
-  FFCA_TRY(st.in(y, size_t(U) * I * N * F * cs, &dy));
-  FFCA_TRY(st.in(P0, size_t(nb) * I * I * cs, &dP));
-  FFCA_TRY(st.in(lam0, size_t(U) * J * F * I * rs, &dl));
-  FFCA_TRY(st.in(v0, size_t(U) * J * N * F * rs, &dv));
-  if (vf_mode == 1) FFCA_TRY(st.in(vf, size_t(nb) * rs, &dvf));
-  if (vf_mode == 2) FFCA_TRY(st.in(vf, size_t(U) * J * N * F * rs, &dvf));
+  FFCA_TRY(st.in(y, size_t(U) * I * N * F * cs, &d.y));
+  FFCA_TRY(st.in(P0, size_t(nb) * I * I * cs, &d.P0));
+  FFCA_TRY(st.in(lam0, size_t(U) * J * F * I * rs, &d.lam0));
+  FFCA_TRY(st.in(v0, size_t(U) * J * N * F * rs, &d.v0));
+  if (vf_mode == 1) FFCA_TRY(st.in(vf, size_t(nb) * rs, &d.vf));
+  if (vf_mode == 2) FFCA_TRY(st.in(vf, size_t(U) * J * N * F * rs, &d.vf));
   void *oP, *ol, *ov, *ovf = nullptr, *oll = nullptr;
   FFCA_TRY(st.out(P_out, size_t(nb) * I * I * cs, &oP));
   FFCA_TRY(st.out(lam_out, size_t(U) * J * F * I * rs, &ol));
@@ -166,50 +410,10 @@ static int loop_entry(int device, void* stream, int mem, int dtype, int U, int I
   FFCA_TRY(st.scratch(size_t(nb) * 4, &dstatus));
   FFCA_CK(cudaMemsetAsync(dstatus, 0, size_t(nb) * 4, s));
   if (record_likelihood) FFCA_TRY(st.scratch(size_t(nb) * nev * 8, &dllb));
-
-  int optin = 0;
-  FFCA_CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-  LoopPlan p;
-  FFCA_TRY(plan_loop(dtype, I, J, N, nb, vf_mode, p, size_t(optin)));
-  void* scratch = nullptr;
-  if (!p.resident) FFCA_TRY(st.scratch(size_t(p.grid) * p.slab, &scratch));
-
-  LoopArgs a;
-  a.U = U; a.I = I; a.J = J; a.N = N; a.F = F;
-  a.total_bins = nb;
-  a.G = p.G; a.C = p.C; a.NL = p.NL;
-  a.iters = iterations; a.K = inner_iterations; a.p_only = p_only;
-  a.vf_mode = vf_mode; a.vf_scalar = vf_scalar; a.vf = dvf;
-  a.y = dy; a.P_in = dP; a.lam_in = dl; a.v_in = dv;
-  a.P_out = oP; a.lam_out = ol; a.v_out = ov;
-  a.vf_out = (double*)ovf;
-  a.ll = (double*)dllb;
-  a.status = (int*)dstatus;
-  a.scratch = scratch;
-  a.slab_bytes = (long long)p.slab;
-
-  LoopFn fn = dtype == FFCA_C64 ? loop_kernel_f32(I, J, p.G, p.resident) : loop_kernel_f64(I, J, p.G, p.resident);
-  if (!fn) {
-    set_error("no kernel for I=%d J=%d", I, J);
-    return FFCA_E_UNSUPPORTED;
-  }
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  if (timing_enabled()) {
-    FFCA_CK(cudaEventCreate(&ev0));
-    FFCA_CK(cudaEventCreate(&ev1));
-    FFCA_CK(cudaEventRecord(ev0, s));
-  }
-  FFCA_TRY(launch_loop(fn, p, a, s));
-  FFCA_CK(cudaGetLastError());
-  if (ev0) {
-    FFCA_CK(cudaEventRecord(ev1, s));
-    FFCA_CK(cudaEventSynchronize(ev1));
-    float ms = 0.f;
-    FFCA_CK(cudaEventElapsedTime(&ms, ev0, ev1));
-    set_kernel_ms(ms);
-    cudaEventDestroy(ev0);
-    cudaEventDestroy(ev1);
-  }
+  d.P = oP; d.lam = ol; d.v = ov; d.vf_out = (double*)ovf;
+  d.ll_bins = (double*)dllb;
+  d.status = (int*)dstatus;
+  FFCA_TRY(launch_problem(device, d, s));
   if (oll) FFCA_TRY(reduce_ll((const double*)dllb, (double*)oll, U, F, nev, -double(N) * F * I * std::log(M_PI), s));
   FFCA_TRY(st.flush());
   return finish_status((const int*)dstatus, status, nb, mem, s, FFCA_ST_SINGULAR_P | FFCA_ST_SINGULAR_B);

@@ -34,13 +34,18 @@ void set_kernel_ms(float ms);
     if (rc_ != FFCA_OK) return rc_; \
   } while (0)
 
+void retain_pool(int dev);
+
 // Selects `device` for the lifetime of the object, restoring the previous one.
+// Also makes the device's stream-ordered pool keep its memory between calls
+// (release threshold = max) so repeated calls do not re-map their buffers.
 struct DeviceGuard {
   int prev = -1;
   bool ok = false;
   explicit DeviceGuard(int dev) {
     if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
     ok = cudaSetDevice(dev) == cudaSuccess;
+    if (ok) retain_pool(dev);
   }
   ~DeviceGuard() {
     if (prev >= 0) cudaSetDevice(prev);

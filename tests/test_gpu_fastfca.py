@@ -320,3 +320,23 @@ def test_launch_count_is_one_kernel():
     y, P0, lam0, v0, _ = mixture(12, 3, 3, 16, 40)
     fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=20)
     assert _lib.launches() == 1
+
+
+@pytest.mark.parametrize("shape", [(5, 3, 3, 40, 70), (1, 4, 4, 37, 300)])
+def test_pipelined_host_call_is_bitwise_one_launch(shape):
+    U, I, J, F, N = shape
+    ys, Ps, ls, vs = [], [], [], []
+    for u in range(U):
+        y, P0, lam0, v0, _ = mixture(200 + u, I, J, F, N, 4)
+        ys.append(y), Ps.append(P0), ls.append(lam0), vs.append(v0)
+    args = (np.stack(ys), np.stack(Ps), np.stack(ls), np.stack(vs))
+    os.environ["FFCA_NO_PIPELINE"] = "1"
+    ref = fastfca.run_fastfca_batch(*args, iterations=3, record_likelihood=True)
+    os.environ.pop("FFCA_NO_PIPELINE")
+    os.environ["FFCA_PIPELINE_MIN_BYTES"] = "1"
+    try:
+        got = fastfca.run_fastfca_batch(*args, iterations=3, record_likelihood=True)
+    finally:
+        os.environ.pop("FFCA_PIPELINE_MIN_BYTES")
+    for a, b in zip(got, ref):
+        assert np.array_equal(a, b)
