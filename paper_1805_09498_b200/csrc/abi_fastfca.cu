@@ -19,9 +19,10 @@ static bool hot_shape(int I, int J) {
 }
 
 static int host_vmax(int I, int JM) {
-  int IC = (I * I * I <= 64) ? I : ((64 / (I * I)) > 0 ? (64 / (I * I)) : 1);
-  int NB = IC * I * I;
-  int va = JM * (1 + I) + 1;
+  const int va = JM * (1 + I) + 1;
+  if (I > 4) return va > I * I * I + 1 ? va : I * I * I + 1;  // group-mode phase B
+  const int IC = (I * I * I <= 64) ? I : ((64 / (I * I)) > 0 ? (64 / (I * I)) : 1);
+  const int NB = IC * I * I;
   return va > NB + 1 ? va : NB + 1;
 }
 
@@ -35,11 +36,12 @@ struct LoopPlan {
 // Slab budget per CTA: two CTAs per SM fit in the 228 KB shared memory.
 static constexpr size_t kSlabBudget = 96 * 1024;
 
-static int choose_threads(int G, int NL) {
+static int choose_threads(int G, int NL, int I) {
   const int per_bin = (NL + 3) / 4;  // ~4 frames per thread per pass (capped at 256 threads)
   int t = G * per_bin;
   t = (t + 31) / 32 * 32;
-  if (t < 64) t = 64;
+  const int tmin = I > 4 ? (8 * (I + 1) + 31) / 32 * 32 : 64;  // I > 4: 8-lane solver groups
+  if (t < tmin) t = tmin;
   if (t > 256) t = 256;
   return t;
 }
@@ -50,12 +52,12 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
   const int JM = hot_shape(I, J) ? J : 8;
   const int VMAX = host_vmax(I, JM);
   // lane-interleaved bin groups only for the exact-J instantiations
-  const int G0 = hot_shape(I, J) ? (dtype == FFCA_C64 ? 4 : 2) : 1;
+  const int G0 = (hot_shape(I, J) && I <= 4) ? (dtype == FFCA_C64 ? 4 : 2) : 1;
   auto fill = [&](int G, int C, bool res) {
     p.G = G;
     p.C = C;
     p.NL = (N + C - 1) / C;
-    p.threads = choose_threads(G, p.NL);
+    p.threads = choose_threads(G, p.NL, I);
     p.resident = res;
     LoopSmem L(I, J, G, p.NL, p.threads / 32, rsz, vf_mode, res, VMAX);
     p.smem = L.total;
@@ -70,7 +72,7 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
     if (nf >= 3 && (G == 1 || G == G0) && (G == 1 || res) && C >= 1 && C <= 8 && (C & (C - 1)) == 0 && C <= N &&
         (C == 1 || G == 1)) {
       fill(G, C, res != 0);
-      if (nf == 4 && thr >= 64 && thr <= 256 && thr % 32 == 0) {
+      if (nf == 4 && thr >= 64 && thr <= 256 && thr % 32 == 0 && (I <= 4 || thr >= 8 * (I + 1))) {
         p.threads = thr;
         LoopSmem L(I, J, G, p.NL, thr / 32, rsz, vf_mode, res != 0, VMAX);
         p.smem = L.total;

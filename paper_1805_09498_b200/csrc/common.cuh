@@ -324,6 +324,68 @@ struct SmallLDL {
   }
 };
 
+// ------------------------------------------------------------------------
+// Gauss-Jordan elimination with partial pivoting on [A | E] by a group of 8
+// consecutive lanes; lane r < I owns row r (fp64, registers).  The pivot at
+// step k is the remaining row with the largest |re|+|im| in column k (lowest
+// lane on ties) -- the same pivot sequence as LAPACK's LU with partial
+// pivoting, so "exactly zero pivot" means what numpy.linalg.inv reports as
+// singular.  Rows are not swapped: on return lane r holds row `k_of_row` of
+// A^-1 E.  `srow` is 2*I double2 of shared scratch for this group.
+// ------------------------------------------------------------------------
+template <int I>
+__device__ __forceinline__ bool gj_group(double2 (&a)[I], double2 (&e)[I], int r, unsigned gmask, double2* srow,
+                                         int& k_of_row, double& logabsdet) {
+  bool used = r >= I;
+  bool ok = true;
+  logabsdet = 0.0;
+  k_of_row = -1;
+#pragma unroll
+  for (int k = 0; k < I; ++k) {
+    double best = used ? -1.0 : cabs1(a[k]);
+    int who = r;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const double ob = __shfl_xor_sync(gmask, best, o);
+      const int ow = __shfl_xor_sync(gmask, who, o);
+      if (ob > best || (ob == best && ow < who)) { best = ob; who = ow; }
+    }
+    const bool piv = (who == r);
+    if (!(best > 0.0)) ok = false;  // exactly zero (or no) pivot
+    if (piv) {
+      const double2 d = a[k];
+      logabsdet += log(hypot(d.x, d.y));
+      const double2 inv = crecip(d);
+#pragma unroll
+      for (int c = 0; c < I; ++c) {
+        a[c] = cmul(a[c], inv);
+        e[c] = cmul(e[c], inv);
+        srow[c] = a[c];
+        srow[I + c] = e[c];
+      }
+      used = true;
+      k_of_row = k;
+    }
+    __syncwarp(gmask);
+    if (!piv && r < I) {
+      const double2 f = a[k];
+#pragma unroll
+      for (int c = 0; c < I; ++c) {
+        const double2 pa = srow[c], pe = srow[I + c];
+        a[c].x -= f.x * pa.x - f.y * pa.y;
+        a[c].y -= f.x * pa.y + f.y * pa.x;
+        e[c].x -= f.x * pe.x - f.y * pe.y;
+        e[c].y -= f.x * pe.y + f.y * pe.x;
+      }
+    }
+    __syncwarp(gmask);
+  }
+  // the pivot lane's log|pivot| terms sum to log|det A|
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) logabsdet += __shfl_xor_sync(gmask, logabsdet, o);
+  return ok;
+}
+
 // Status bits written per bin (mapped to the reference's exceptions on host).
 enum : int {
   ST_SINGULAR_P = 1,          // errors.SingularP               (fastfca.py:360-363)

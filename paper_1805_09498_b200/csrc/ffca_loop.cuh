@@ -63,11 +63,18 @@ struct Shape {
   static constexpr int NB = IC * I * I;  // reals per chunk
   static constexpr bool PREG = I <= 4;   // keep P / lambda in registers
   static constexpr int RS = odd_up(I);   // complex per slab record
+  // I > 4: the I^3 B accumulators are spread over groups of 8 lanes per point
+  static constexpr bool GROUPB = I > 4;
+  static constexpr int NCX = I * (I - 1) / 2;        // complex off-diagonal entries
+  static constexpr int NSL = (NCX + 7) / 8;          // complex entries per lane
+  static constexpr int NVG = (1 + 2 * NSL) * I + 1;  // values per lane (+ likelihood)
 };
 
 template <int I, int JM>
 __host__ __device__ constexpr int loop_vmax() {
-  return (JM * (1 + I) + 1) > (Shape<I>::NB + 1) ? (JM * (1 + I) + 1) : (Shape<I>::NB + 1);
+  return Shape<I>::GROUPB
+             ? ((JM * (1 + I) + 1) > (I * I * I + 1) ? (JM * (1 + I) + 1) : (I * I * I + 1))
+             : ((JM * (1 + I) + 1) > (Shape<I>::NB + 1) ? (JM * (1 + I) + 1) : (Shape<I>::NB + 1));
 }
 
 // Shared-memory carve-up; identical on host (sizing) and device.
@@ -102,7 +109,11 @@ struct LoopSmem {
     cpart = o; o += align16(size_t(2) * G * VMAX * 8);
     tot = o;   o += align16(size_t(G) * VMAX * 8);
     bst = o;   o += align16(size_t(G) * I * I * I * 8);
-    M = o;     o += align16(size_t(G) * (I + 1) * I * I * 16);
+    {  // solver workspace: per-system matrices (I <= 4) or B_i^-1 + group rows (I > 4)
+      const size_t m1 = size_t(G) * (I + 1) * I * I * 16, m2 = (size_t(I) * I * I + 2 * I * (I + 1)) * 16;
+      M = o;
+      o += align16(m1 > m2 ? m1 : m2);
+    }
     rhs = o;   o += align16(size_t(G) * (I + 1) * I * 16);
     piv = o;   o += align16(size_t(G) * (I + 1) * I * 4);
     total = o;
@@ -124,21 +135,18 @@ __device__ __forceinline__ T bin_warp_sum(T x) {
 // rank order.  cpart is double-buffered (parity) so a fast CTA cannot
 // overwrite partials a slower CTA is still reading over DSMEM.
 // ------------------------------------------------------------------------
-template <typename R, int V, int G>
-__device__ __forceinline__ void bin_reduce(const R (&vals)[V], double* wpart, double* cpart, double* tot, int C,
-                                           int VMAX, int& parity) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, W = blockDim.x >> 5;
-  const int g = lane % G;
-#pragma unroll
-  for (int k = 0; k < V; ++k) {
-    const R s = bin_warp_sum<G>(vals[k]);
-    if (lane < G) wpart[(warp * G + g) * VMAX + k] = double(s);
-  }
+// Block / cluster half of the reduction: wpart[(warp*G + g)*VMAX + k] holds each
+// warp's partial for k < nv; sums over warps in index order, then cluster
+// ranks in rank order, into tot[g*VMAX + k].
+template <int G>
+__device__ __forceinline__ void bin_reduce_tail(int nv, double* wpart, double* cpart, double* tot, int C, int VMAX,
+                                                int& parity) {
+  const int tid = threadIdx.x, W = blockDim.x >> 5;
   __syncthreads();
   double* cp = cpart + parity * G * VMAX;
   double* dst = (C > 1) ? cp : tot;
-  for (int t = tid; t < G * V; t += blockDim.x) {
-    const int gg = t / V, k = t % V;
+  for (int t = tid; t < G * nv; t += blockDim.x) {
+    const int gg = t / nv, k = t % nv;
     double s = 0.0;
     for (int w = 0; w < W; ++w) s += wpart[(w * G + gg) * VMAX + k];
     dst[gg * VMAX + k] = s;
@@ -146,8 +154,8 @@ __device__ __forceinline__ void bin_reduce(const R (&vals)[V], double* wpart, do
   if (C > 1) {
     cg::cluster_group cl = cg::this_cluster();
     cl.sync();
-    for (int t = tid; t < G * V; t += blockDim.x) {
-      const int gg = t / V, k = t % V;
+    for (int t = tid; t < G * nv; t += blockDim.x) {
+      const int gg = t / nv, k = t % nv;
       double s = 0.0;
       for (int r = 0; r < C; ++r) s += cl.map_shared_rank(cp, r)[gg * VMAX + k];
       tot[gg * VMAX + k] = s;
@@ -155,6 +163,19 @@ __device__ __forceinline__ void bin_reduce(const R (&vals)[V], double* wpart, do
     parity ^= 1;
   }
   __syncthreads();
+}
+
+template <typename R, int V, int G>
+__device__ __forceinline__ void bin_reduce(const R (&vals)[V], double* wpart, double* cpart, double* tot, int C,
+                                           int VMAX, int& parity) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane % G;
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const R s = bin_warp_sum<G>(vals[k]);
+    if (lane < G) wpart[(warp * G + g) * VMAX + k] = double(s);
+  }
+  bin_reduce_tail<G>(V, wpart, cpart, tot, C, VMAX, parity);
 }
 
 // Per-point work of one thread over its frames of one bin (registers only).
@@ -319,6 +340,75 @@ struct PointWork {
     }
   }
 
+  // Phase B for I > 4: lanes with the same (bin g, group q) cooperate on one
+  // point; lane position p = 0..7 owns the diagonal entry (p, p) and the
+  // complex entries c = p, p+8, ... of the packed lower triangle, for all i,
+  // so every product y_x conj(y_y) is formed once and each lane holds at most
+  // (1 + 2*NSL)*I accumulators.  Each lane forms 1/w_p and broadcasts it.
+  static constexpr int NSL = Shape<I>::NSL, NVG = Shape<I>::NVG;
+  template <bool REC>
+  __device__ __forceinline__ void phaseB_group(R (&acc)[NVG], int NLr, bool active, const int (&cx)[NSL ? NSL : 1],
+                                               const int (&cy)[NSL ? NSL : 1]) const {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
+    constexpr int QW = 4 / G;  // point groups per bin per warp
+    const int p = (lane / G) % 8, q = lane / (8 * G);
+    const int start = warp * QW + q, stride = W * QW;
+    const int src0 = q * 8 * G + g;
+    // warp-uniform trip count (every lane must reach the shuffles); lanes whose
+    // point is out of range, or whose bin is padding, contribute nothing
+    const int trips = (NLr > warp * QW) ? (NLr - warp * QW + stride - 1) / stride : 0;
+#pragma unroll 1
+    for (int k = 0; k < trips; ++k) {
+      const int n = start + k * stride;
+      const bool valid = active && n < NLr;
+      const int nn = valid ? n : 0;
+      const C2* yp = ys + (nn * G + g) * RS;
+      const R* vp = vs + (nn * G + g) * JS;
+      R iw_own = R(0);
+      if (valid && p < I) {
+        R s = R(0);
+#pragma unroll
+        for (int j = 0; j < JM; ++j)
+          if (j < J) s = fma(vp[j], Lam(j, p), s);
+        iw_own = rcp(fmax(s, wfl));
+      }
+      R iw[I];
+#pragma unroll
+      for (int i = 0; i < I; ++i) iw[i] = __shfl_sync(FULL, iw_own, src0 + i * G);
+      if (valid && p < I) {
+        const C2 yd = yp[p];
+        const R dv = yd.x * yd.x + yd.y * yd.y;
+#pragma unroll
+        for (int i = 0; i < I; ++i) acc[i] = fma(dv, iw[i], acc[i]);
+      }
+#pragma unroll
+      for (int s = 0; s < NSL; ++s) {
+        if (valid && p + 8 * s < Shape<I>::NCX) {
+          const C2 a = yp[cx[s]], b = yp[cy[s]];
+          const R re = a.x * b.x + a.y * b.y, im = a.y * b.x - a.x * b.y;
+#pragma unroll
+          for (int i = 0; i < I; ++i) {
+            acc[(1 + 2 * s) * I + i] = fma(re, iw[i], acc[(1 + 2 * s) * I + i]);
+            acc[(2 + 2 * s) * I + i] = fma(im, iw[i], acc[(2 + 2 * s) * I + i]);
+          }
+        }
+      }
+      if constexpr (REC) {
+        if (valid && p == 0) {
+          C2 yv[I];
+#pragma unroll
+          for (int i = 0; i < I; ++i) yv[i] = yp[i];
+          R q2[I];
+          transform_q(yv, q2);
+          R l = R(0);
+#pragma unroll
+          for (int i = 0; i < I; ++i) l += flog(R(1) / iw[i]) + q2[i] * iw[i];
+          acc[NVG - 1] += l;
+        }
+      }
+    }
+  }
+
   // Likelihood partial sum_n,i ln w + q / w at the current state.
   __device__ __forceinline__ void phaseL(R (&acc)[1]) const {
     const C2* yp = ys + rec0 * RS;
@@ -337,7 +427,7 @@ struct PointWork {
 };
 
 template <typename R, int I, int JT, int G, bool RES>
-__global__ void __launch_bounds__(256, 2) ffca_loop_kernel(const LoopArgs a) {
+__global__ void __launch_bounds__(256, (I > 4 ? 1 : 2)) ffca_loop_kernel(const LoopArgs a) {
   using C2 = typename Cpx<R>::T;
   constexpr int JM = JT > 0 ? JT : 8;
   constexpr int IC = Shape<I>::IC, NCH = Shape<I>::NCH, NB = Shape<I>::NB;
@@ -483,6 +573,23 @@ __global__ void __launch_bounds__(256, 2) ffca_loop_kernel(const LoopArgs a) {
   pw.g = g; pw.J = J; pw.JS = JS; pw.rec0 = rec0; pw.rstep = rstep; pw.npts = npts;
   pw.wfl = wfl; pw.invI = invI;
 
+  // complex off-diagonal entries (x, y < x) owned by this lane in group-mode phase B
+  int gcx[Shape<I>::NSL ? Shape<I>::NSL : 1], gcy[Shape<I>::NSL ? Shape<I>::NSL : 1];
+  if constexpr (Shape<I>::GROUPB) {
+    const int p = ((tid & 31) / G) % 8;
+#pragma unroll
+    for (int s = 0; s < Shape<I>::NSL; ++s) {
+      const int c = p + 8 * s;
+      int x = 1;
+      while ((x + 1) * x / 2 <= c) ++x;
+      gcx[s] = x;
+      gcy[s] = c - x * (x - 1) / 2;
+      if (c >= Shape<I>::NCX) gcx[s] = gcy[s] = 0;
+    }
+  } else {
+    gcx[0] = gcy[0] = 0;
+  }
+
   // ======================= outer iterations =======================
   for (int it = 0; it < a.iters; ++it) {
     // ---------------- phase A: fused E/M sweep ----------------
@@ -528,6 +635,45 @@ __global__ void __launch_bounds__(256, 2) ffca_loop_kernel(const LoopArgs a) {
     // ---------------- phase B: weighted covariances ----------------
     pw.load_PL();
     double llB = 0.0;
+    if constexpr (Shape<I>::GROUPB) {
+      constexpr int NSL = Shape<I>::NSL, NVG = Shape<I>::NVG;
+      R acc[NVG];
+#pragma unroll
+      for (int kk = 0; kk < NVG; ++kk) acc[kk] = R(0);
+      if (rec) pw.template phaseB_group<true>(acc, NLr, active, gcx, gcy);
+      else pw.template phaseB_group<false>(acc, NLr, active, gcx, gcy);
+      // reduce over the point groups of the warp (lanes differing in q only)
+      const int lane = tid & 31, warp = tid >> 5;
+      const int p = (lane / G) % 8, q = lane / (8 * G);
+#pragma unroll
+      for (int kk = 0; kk < NVG; ++kk) {
+#pragma unroll
+        for (int o = 16; o >= 8 * G; o >>= 1) acc[kk] += __shfl_xor_sync(FULL, acc[kk], o);
+      }
+      if (q == 0) {
+        double* wp = wpart + (warp * G + g) * VMAX;
+        if (p < I)
+#pragma unroll
+          for (int i = 0; i < I; ++i) wp[i * I * I + p * p] = double(acc[i]);
+#pragma unroll
+        for (int s = 0; s < NSL; ++s)
+          if (p + 8 * s < Shape<I>::NCX) {
+            const int e = gcx[s] * gcx[s] + 1 + 2 * gcy[s];
+#pragma unroll
+            for (int i = 0; i < I; ++i) {
+              wp[i * I * I + e] = double(acc[(1 + 2 * s) * I + i]);
+              wp[i * I * I + e + 1] = double(acc[(2 + 2 * s) * I + i]);
+            }
+          }
+        if (p == 0) wp[I * I * I] = double(acc[NVG - 1]);
+      }
+      bin_reduce_tail<G>(I * I * I + 1, wpart, cpart, tot, C, VMAX, parity);
+      if (rec && tid < G) llB = tot[tid * VMAX + I * I * I];
+      for (int t = tid; t < G * I * I * I; t += blockDim.x) {
+        const int gg = t / (I * I * I), kk = t % (I * I * I);
+        bst[gg * I * I * I + kk] = tot[gg * VMAX + kk];
+      }
+    } else {
 #pragma unroll 1
     for (int ch = 0; ch < NCH; ++ch) {
       R acc[NB + 1];
@@ -543,6 +689,7 @@ __global__ void __launch_bounds__(256, 2) ffca_loop_kernel(const LoopArgs a) {
         const int gg = t / nbc, kk = t % nbc;
         bst[gg * I * I * I + ch * NB + kk] = tot[gg * VMAX + kk];
       }
+    }
     }
     __syncthreads();
 
@@ -627,60 +774,76 @@ __global__ void __launch_bounds__(256, 2) ffca_loop_kernel(const LoopArgs a) {
         __syncthreads();
       }
     } else {
-      // I > 4: one thread per system on shared-memory matrices.
-      const int s = tid % (I + 1);
-      const int gg = tid / (I + 1);
-      const long long b = group * G + gg;
-      const bool bact = gg < G && b < a.total_bins;
-      double2* Ms = Msys + (gg * (I + 1) + s) * I * I;
-      int* pv = pivs + (gg * (I + 1) + s) * I;
-      double2* rv = rhsv + (gg * (I + 1) + s) * I;
-      if (bact && s > 0) {
-        const int i = s - 1;
-        const double* T = bst + gg * I * I * I + i * I * I;
+      // I > 4: one group of 8 lanes per system (G == 1).  Group 0 inverts P,
+      // groups 1..I invert B_i, all concurrently (Gauss-Jordan, row per lane);
+      // then group 1+i applies B_i^-1 to [P^-H]_i.
+      static_assert(G == 1, "I > 4 runs one bin per CTA");
+      const int m = tid >> 3, r = tid & 7;
+      const unsigned gmask = 0xFFu << (8 * ((tid >> 3) & 3));
+      const bool bact = (m <= I) && active;
+      double2* Binv = Msys;                         // I x I x I  (row-major per i)
+      double2* srow = Msys + I * I * I + m * 2 * I;  // group scratch
+      if (m >= 1 && m <= I) {
+        const int i = m - 1;
+        const double* T = bst + i * I * I;
         double tr = 0.0;
+#pragma unroll
+        for (int x = 0; x < I; ++x) tr += T[x * x] * invN;
         for (int pass = 0; pass < 2; ++pass) {
-          int kk = 0;
-          for (int x = 0; x < I; ++x) {
-            const double dd = T[kk++] * invN;
-            Ms[x * I + x] = make_double2(dd + (pass ? 1e-10 * tr : 0.0), 0.0);
-            if (!pass) tr += dd;
-            for (int y2 = 0; y2 < x; ++y2) {
-              const double re = T[kk++] * invN, im = T[kk++] * invN;
-              Ms[x * I + y2] = make_double2(re, im);
-              Ms[y2 * I + x] = make_double2(re, -im);
+          double2 ar[I], er[I];
+#pragma unroll
+          for (int c = 0; c < I; ++c) {
+            er[c] = make_double2(c == r ? 1.0 : 0.0, 0.0);
+            if (r >= I) { ar[c] = make_double2(0.0, 0.0); continue; }
+            const int hi = r >= c ? r : c, lo = r >= c ? c : r;
+            if (hi == lo) ar[c] = make_double2(T[hi * hi] * invN + (pass ? 1e-10 * tr : 0.0), 0.0);
+            else {
+              const double re = T[hi * hi + 1 + 2 * lo] * invN, im = T[hi * hi + 2 + 2 * lo] * invN;
+              ar[c] = make_double2(re, r >= c ? im : -im);
             }
           }
-          const bool okB = lu_factor<I>(Ms, pv);
-          if (okB && pass == 0) break;
-          if (pass == 1 && crank == 0) atomicOr(&a.status[b], okB ? ST_B_LOADED : ST_SINGULAR_B);
+          int krow;
+          double ld;
+          const bool ok = gj_group<I>(ar, er, r, gmask, srow, krow, ld);
+          if (ok || pass == 1) {
+            if (r < I)
+#pragma unroll
+              for (int c = 0; c < I; ++c) Binv[(i * I + krow) * I + c] = er[c];
+            if (pass == 1 && r == 0 && bact && crank == 0) atomicOr(&a.status[group], ok ? ST_B_LOADED : ST_SINGULAR_B);
+            break;
+          }
         }
       }
 #pragma unroll 1
       for (int k = 0; k < a.K; ++k) {
-        if (bact && s == 0) {
-          for (int e = 0; e < I * I; ++e) Ms[e] = Pd[gg * I * I + e];
-          const bool okP = lu_factor<I>(Ms, pv);
-          if (!okP && crank == 0) atomicOr(&a.status[b], ST_SINGULAR_P);
-          if (k == 0) ldet[gg] = lu_logabsdet<I>(Ms);
+        if (m == 0) {
+          double2 ar[I], er[I];
+#pragma unroll
           for (int c = 0; c < I; ++c) {
-            for (int x = 0; x < I; ++x) rv[x] = make_double2(x == c ? 1.0 : 0.0, 0.0);
-            lu_solve<I>(Ms, pv, rv);
-            for (int x = 0; x < I; ++x) Pinv[(gg * I + x) * I + c] = rv[x];
+            ar[c] = r < I ? Pd[r * I + c] : make_double2(0.0, 0.0);
+            er[c] = make_double2(c == r ? 1.0 : 0.0, 0.0);
           }
+          int krow;
+          double ld;
+          const bool ok = gj_group<I>(ar, er, r, gmask, srow, krow, ld);
+          if (!ok && r == 0 && bact && crank == 0) atomicOr(&a.status[group], ST_SINGULAR_P);
+          if (k == 0 && r == 0) ldet[0] = ld;
+          if (r < I)
+#pragma unroll
+            for (int c = 0; c < I; ++c) Pinv[krow * I + c] = er[c];
         }
         __syncthreads();
-        if (bact && s > 0) {
-          const int i = s - 1;
-          for (int x = 0; x < I; ++x) {
-            const double2 z = Pinv[(gg * I + i) * I + x];
-            rv[x] = make_double2(z.x, -z.y);  // [P^-H]_{x,i} = conj(P^-1_{i,x})
+        if (m >= 1 && m <= I && r < I) {
+          const int i = m - 1;
+          double2 x = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int c = 0; c < I; ++c) {  // (B_i^-1)_{r,c} conj(P^-1_{i,c})
+            const double2 bq = Binv[(i * I + r) * I + c], pq = Pinv[i * I + c];
+            x.x += bq.x * pq.x + bq.y * pq.y;
+            x.y += bq.y * pq.x - bq.x * pq.y;
           }
-          lu_solve<I>(Ms, pv, rv);
-          for (int x = 0; x < I; ++x) {
-            Pd[(gg * I + x) * I + i] = rv[x];
-            Pc[(gg * I + x) * I + i] = mk<C2, R>(R(rv[x].x), R(rv[x].y));
-          }
+          Pd[r * I + i] = x;
+          Pc[r * I + i] = mk<C2, R>(R(x.x), R(x.y));
         }
         __syncthreads();
       }

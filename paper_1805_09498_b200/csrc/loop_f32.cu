@@ -10,7 +10,9 @@ using LoopFn = void (*)(const LoopArgs);
 // global-slab path.
 template <int I, int J>
 static LoopFn hot(int G, bool res) {
-  if (G == 4 && res) return ffca_loop_kernel<float, I, J, 4, true>;
+  if constexpr (I <= 4) {
+    if (G == 4 && res) return ffca_loop_kernel<float, I, J, 4, true>;
+  }
   if (G == 1) return res ? (LoopFn)ffca_loop_kernel<float, I, J, 1, true> : (LoopFn)ffca_loop_kernel<float, I, J, 1, false>;
   return nullptr;
 }
