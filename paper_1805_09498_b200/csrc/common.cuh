@@ -333,14 +333,24 @@ struct SmallLDL {
 // singular.  Rows are not swapped: on return lane r holds row `k_of_row` of
 // A^-1 E.  `srow` is 2*I double2 of shared scratch for this group.
 // ------------------------------------------------------------------------
-template <int I>
+// Reciprocal of a complex number via rcp.approx + Newton (no IEEE division).
+__device__ __forceinline__ double2 crecip_fast(const double2 z) {
+  const double m = fmax(fabs(z.x), fabs(z.y));
+  if (m > 0x1p-500 && m < 0x1p500) {
+    const double r = rcp(z.x * z.x + z.y * z.y);
+    return make_double2(z.x * r, -z.y * r);
+  }
+  return crecip(z);
+}
+
+template <int I, bool LOGDET>
 __device__ __forceinline__ bool gj_group(double2 (&a)[I], double2 (&e)[I], int r, unsigned gmask, double2* srow,
                                          int& k_of_row, double& logabsdet) {
   bool used = r >= I;
   bool ok = true;
   logabsdet = 0.0;
   k_of_row = -1;
-#pragma unroll
+#pragma unroll 1
   for (int k = 0; k < I; ++k) {
     double best = used ? -1.0 : cabs1(a[k]);
     int who = r;
@@ -354,8 +364,8 @@ __device__ __forceinline__ bool gj_group(double2 (&a)[I], double2 (&e)[I], int r
     if (!(best > 0.0)) ok = false;  // exactly zero (or no) pivot
     if (piv) {
       const double2 d = a[k];
-      logabsdet += log(hypot(d.x, d.y));
-      const double2 inv = crecip(d);
+      if (LOGDET) logabsdet += log(hypot(d.x, d.y));
+      const double2 inv = crecip_fast(d);
 #pragma unroll
       for (int c = 0; c < I; ++c) {
         a[c] = cmul(a[c], inv);
@@ -380,9 +390,10 @@ __device__ __forceinline__ bool gj_group(double2 (&a)[I], double2 (&e)[I], int r
     }
     __syncwarp(gmask);
   }
-  // the pivot lane's log|pivot| terms sum to log|det A|
+  // the pivot lanes' log|pivot| terms sum to log|det A|
+  if (LOGDET)
 #pragma unroll
-  for (int o = 1; o < 8; o <<= 1) logabsdet += __shfl_xor_sync(gmask, logabsdet, o);
+    for (int o = 1; o < 8; o <<= 1) logabsdet += __shfl_xor_sync(gmask, logabsdet, o);
   return ok;
 }
 

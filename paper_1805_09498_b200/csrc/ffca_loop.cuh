@@ -804,7 +804,7 @@ __global__ void __launch_bounds__(256, (I > 4 ? 1 : 2)) ffca_loop_kernel(const L
           }
           int krow;
           double ld;
-          const bool ok = gj_group<I>(ar, er, r, gmask, srow, krow, ld);
+          const bool ok = gj_group<I, false>(ar, er, r, gmask, srow, krow, ld);
           if (ok || pass == 1) {
             if (r < I)
 #pragma unroll
@@ -824,8 +824,9 @@ __global__ void __launch_bounds__(256, (I > 4 ? 1 : 2)) ffca_loop_kernel(const L
             er[c] = make_double2(c == r ? 1.0 : 0.0, 0.0);
           }
           int krow;
-          double ld;
-          const bool ok = gj_group<I>(ar, er, r, gmask, srow, krow, ld);
+          double ld = 0.0;
+          const bool ok = (rec && k == 0) ? gj_group<I, true>(ar, er, r, gmask, srow, krow, ld)
+                                          : gj_group<I, false>(ar, er, r, gmask, srow, krow, ld);
           if (!ok && r == 0 && bact && crank == 0) atomicOr(&a.status[group], ST_SINGULAR_P);
           if (k == 0 && r == 0) ldet[0] = ld;
           if (r < I)
