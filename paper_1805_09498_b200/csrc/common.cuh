@@ -64,6 +64,19 @@ __device__ __forceinline__ void cmac_conj(C2& acc, const C2 p, const C2 y) {
   acc.y = fma(p.x, y.y, fma(-p.y, y.x, acc.y));
 }
 
+// Asynchronous global -> shared copy of one element (cp.async, LDGSTS);
+// `valid == false` zero-fills the destination without reading the source.
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem_dst, const void* gsrc, bool valid) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  const int n = valid ? BYTES : 0;
+  if constexpr (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gsrc), "r"(n));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(d), "l"(gsrc), "n"(BYTES), "r"(n));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 // Sum over lanes that share (lane mod G); G is a power of two dividing 32.
 template <typename T>
 __device__ __forceinline__ T warp_sum_seg(T x, int G) {

@@ -485,34 +485,41 @@ __global__ void __launch_bounds__(256, (I > 4 ? 1 : 2)) ffca_loop_kernel(const L
   const R* __restrict__ vg = (const R*)a.v_in;
 
   // ---------------- load: gather (I,N,F) -> slab records ----------------
-  // element e = (i * NL + n) * G + g' with g' fastest: consecutive lanes read
-  // consecutive bins (one 32-byte sector); e % G == tid % G == g.
-  R psum = R(0);
-  for (int e = tid; e < I * NL * G; e += blockDim.x) {
-    const int rest = e / G;
-    const int n = rest % NL, i = rest / NL;
-    C2 val = mk<C2, R>(R(0), R(0));
-    if (active && n < NLr) {
-      val = yg[((u * I + i) * (long long)N + n0 + n) * F + f];
-      psum += val.x * val.x + val.y * val.y;
-    }
-    ys[(n * G + g) * RS + i] = val;
-  }
-  for (int e = tid; e < J * NL * G; e += blockDim.x) {
-    const int rest = e / G;
-    const int n = rest % NL, j = rest / NL;
-    R val = R(0);
-    if (active && n < NLr) val = vg[((u * J + j) * (long long)N + n0 + n) * F + f];
-    vs[(n * G + g) * JS + j] = val;
-  }
-  if (a.vf_mode == 2) {
+  // Consecutive lanes take consecutive bins g of the group, then frames, so a
+  // warp reads whole 32-byte sectors of y[i, n, f..f+G).  Resident slabs are
+  // filled with cp.async (zero-fill for padding), keeping every load of the
+  // thread in flight at once.
+  {
     const R* vfg = (const R*)a.vf;
-    for (int e = tid; e < J * NL * G; e += blockDim.x) {
-      const int rest = e / G;
-      const int n = rest % NL, j = rest / NL;
-      R val = R(0);
-      if (active && n < NLr) val = vfg[((u * J + j) * (long long)N + n0 + n) * F + f];
-      vfs[(n * G + g) * JS + j] = val;
+    if (resident) {
+#pragma unroll 1
+      for (int i = 0; i < I; ++i)
+        for (int n = slot; n < NL; n += nslots) {
+          const bool ok = active && n < NLr;
+          const C2* src = ok ? yg + ((u * I + i) * (long long)N + n0 + n) * F + f : yg;
+          cp_async<sizeof(C2)>(ys + (n * G + g) * RS + i, src, ok);
+        }
+#pragma unroll 1
+      for (int j = 0; j < J; ++j)
+        for (int n = slot; n < NL; n += nslots) {
+          const bool ok = active && n < NLr;
+          const long long off = ((u * J + j) * (long long)N + n0 + n) * F + f;
+          cp_async<sizeof(R)>(vs + (n * G + g) * JS + j, ok ? vg + off : vg, ok);
+          if (a.vf_mode == 2) cp_async<sizeof(R)>(vfs + (n * G + g) * JS + j, ok ? vfg + off : vfg, ok);
+        }
+    } else {
+      for (int i = 0; i < I; ++i)
+        for (int n = slot; n < NL; n += nslots) {
+          const bool ok = active && n < NLr;
+          ys[(n * G + g) * RS + i] = ok ? yg[((u * I + i) * (long long)N + n0 + n) * F + f] : mk<C2, R>(R(0), R(0));
+        }
+      for (int j = 0; j < J; ++j)
+        for (int n = slot; n < NL; n += nslots) {
+          const bool ok = active && n < NLr;
+          const long long off = ((u * J + j) * (long long)N + n0 + n) * F + f;
+          vs[(n * G + g) * JS + j] = ok ? vg[off] : R(0);
+          if (a.vf_mode == 2) vfs[(n * G + g) * JS + j] = ok ? vfg[off] : R(0);
+        }
     }
   }
   for (int t = tid; t < G * I * I; t += blockDim.x) {
@@ -537,10 +544,19 @@ __global__ void __launch_bounds__(256, (I > 4 ? 1 : 2)) ffca_loop_kernel(const L
     lamd[t] = l;
     lamc[t] = R(l);
   }
+  cp_async_wait_all();
   __syncthreads();
 
   // ---------------- v floor per bin (fca.py:82-89 when auto) ----------------
   if (a.vf_mode == 3) {
+    R psum = R(0);
+    if (active)
+      for (int n = slot; n < NLr; n += nslots)
+#pragma unroll
+        for (int i = 0; i < I; ++i) {
+          const C2 z = ys[(n * G + g) * RS + i];
+          psum += z.x * z.x + z.y * z.y;
+        }
     const R pv[1] = {psum};
     bin_reduce<R, 1, G>(pv, wpart, cpart, tot, C, VMAX, parity);
     if (tid < G) {
@@ -878,11 +894,9 @@ __global__ void __launch_bounds__(256, (I > 4 ? 1 : 2)) ffca_loop_kernel(const L
 
   // ---------------- write back ----------------
   R* vo = (R*)a.v_out;
-  for (int e = tid; e < J * NL * G; e += blockDim.x) {
-    const int rest = e / G;
-    const int n = rest % NL, j = rest / NL;
-    if (active && n < NLr) vo[((u * J + j) * (long long)N + n0 + n) * F + f] = vs[(n * G + g) * JS + j];
-  }
+  if (active)
+    for (int j = 0; j < J; ++j)
+      for (int n = slot; n < NLr; n += nslots) vo[((u * J + j) * (long long)N + n0 + n) * F + f] = vs[(n * G + g) * JS + j];
   if (crank == 0) {
     for (int t = tid; t < G * I * I; t += blockDim.x) {
       const long long b = group * G + t / (I * I);
