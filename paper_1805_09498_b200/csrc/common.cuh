@@ -57,6 +57,35 @@ __device__ __forceinline__ C2 mk(R x, R y) {
   return z;
 }
 
+// Pair arithmetic: fp32 pairs lower to Blackwell's packed FFMA2 (fma.rn.f32x2,
+// scalar operands become broadcast operands, swaps become operand swizzles);
+// fp64 pairs are two DFMAs.
+__device__ __forceinline__ unsigned long long pk64(float2 a) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
+}
+__device__ __forceinline__ float2 upk64(unsigned long long r) {
+  float2 a;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+  return a;
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk64(a)), "l"(pk64(b)), "l"(pk64(c)));
+  return upk64(r);
+}
+__device__ __forceinline__ double2 fma2(double2 a, double2 b, double2 c) {
+  return make_double2(fma(a.x, b.x, c.x), fma(a.y, b.y, c.y));
+}
+template <typename R>
+__device__ __forceinline__ typename Cpx<R>::T bc2(R x) {
+  typename Cpx<R>::T t;
+  t.x = x;
+  t.y = x;
+  return t;
+}
+
 // conj(p) * y, accumulated into acc
 template <typename C2>
 __device__ __forceinline__ void cmac_conj(C2& acc, const C2 p, const C2 y) {

@@ -245,99 +245,179 @@ struct PointWork {
   }
 
   // Phase A: fused E/M sweep over this thread's frames (fastfca.py:323-340).
+  // Arithmetic is written on value pairs (fma2 -> FFMA2 for fp32): the
+  // transform as 2 packed MACs per complex term, (r1_j, r2_j) against pairs
+  // (1/w_i, q_i/w_i^2), and s1_j over pairs of i.
   template <bool REC, bool VF2>
   __device__ __forceinline__ void phaseA(R (&acc)[VA], const R vfl_b) {
+    using P2 = C2;
+    constexpr int IP = I / 2;           // i-pairs
+    constexpr bool IODD = (I & 1) != 0;
     const C2* yp = ys + rec0 * RS;
     R* vp = vs + rec0 * JS;
     const R* fp = vfs + rec0 * JS;
+    R s0[JM];
+    P2 s1p[JM][IP > 0 ? IP : 1];
+    R s1s[JM];
+    R lacc = R(0);
+#pragma unroll
+    for (int j = 0; j < JM; ++j) {
+      s0[j] = R(0);
+      s1s[j] = R(0);
+#pragma unroll
+      for (int ip = 0; ip < (IP > 0 ? IP : 1); ++ip) s1p[j][ip] = mk<C2, R>(R(0), R(0));
+    }
 #pragma unroll 1
     for (int k = 0; k < npts; ++k, yp += rstep * RS, vp += rstep * JS, fp += rstep * JS) {
       C2 yv[I];
-      R vj[JM], q[I], w[I], iw[I], qiw2[I], d[I];
+      R vj[JM];
       load_point(yp, vp, yv, vj);
-      transform_q(yv, q);
+      // y_t = P^H y, q = |y_t|^2
+      R q[I];
+#pragma unroll
+      for (int b = 0; b < I; ++b) {
+        P2 t = mk<C2, R>(R(0), R(0));
+#pragma unroll
+        for (int x = 0; x < I; ++x) {
+          const C2 pp = P(x, b);
+          t = fma2(yv[x], bc2<R>(pp.x), t);                                  // p.x (y.x, y.y)
+          t = fma2(mk<C2, R>(yv[x].y, -yv[x].x), bc2<R>(pp.y), t);          // p.y (y.y, -y.x)
+        }
+        q[b] = t.x * t.x + t.y * t.y;
+      }
+      R w[I];
       weights(vj, w);
+      // Qi = (1/w_i, q_i/w_i^2)
+      P2 Q[I];
 #pragma unroll
       for (int i = 0; i < I; ++i) {
-        iw[i] = rcp(w[i]);
-        qiw2[i] = (q[i] * iw[i]) * iw[i];
-        d[i] = qiw2[i] - iw[i];
+        const R iw = rcp(w[i]);
+        Q[i] = mk<C2, R>(iw, (q[i] * iw) * iw);
       }
       if constexpr (REC) {
-        R l = R(0);
 #pragma unroll
-        for (int i = 0; i < I; ++i) l += flog(w[i]) + q[i] * iw[i];
-        acc[VA - 1] += l;
+        for (int i = 0; i < I; ++i) lacc += flog(w[i]) + q[i] * Q[i].x;
       }
+      R d[I];
+#pragma unroll
+      for (int i = 0; i < I; ++i) d[i] = Q[i].y - Q[i].x;
 #pragma unroll
       for (int j = 0; j < JM; ++j) {
         if (j < J) {
-          R r1 = R(0), r2 = R(0);
+          P2 rr = mk<C2, R>(R(0), R(0));  // (r1_j, r2_j)
 #pragma unroll
-          for (int i = 0; i < I; ++i) {
-            r1 = fma(iw[i], Lam(j, i), r1);
-            r2 = fma(qiw2[i], Lam(j, i), r2);
-          }
+          for (int i = 0; i < I; ++i) rr = fma2(Q[i], bc2<R>(Lam(j, i)), rr);
           const R v = vj[j];
-          const R step = (((r1 - r2) * v) * v) * invI;
+          const R step = (((rr.x - rr.y) * v) * v) * invI;
           R fl = vfl_b;
           if constexpr (VF2) fl = fp[j];
           const R vn = fmax(v - step, fl);
           const R ratio = v * rcp(vn);
-          acc[j] += ratio;
+          s0[j] += ratio;
           const R rv = ratio * v;
 #pragma unroll
-          for (int i = 0; i < I; ++i) acc[JM + j * I + i] = fma(rv, d[i], acc[JM + j * I + i]);
+          for (int ip = 0; ip < IP; ++ip) s1p[j][ip] = fma2(bc2<R>(rv), mk<C2, R>(d[2 * ip], d[2 * ip + 1]), s1p[j][ip]);
+          if constexpr (IODD) s1s[j] = fma(rv, d[I - 1], s1s[j]);
           vp[j] = vn;
         }
       }
     }
+#pragma unroll
+    for (int j = 0; j < JM; ++j) {
+      acc[j] = s0[j];
+#pragma unroll
+      for (int ip = 0; ip < IP; ++ip) {
+        acc[JM + j * I + 2 * ip] = s1p[j][ip].x;
+        acc[JM + j * I + 2 * ip + 1] = s1p[j][ip].y;
+      }
+      if constexpr (IODD) acc[JM + j * I + I - 1] = s1s[j];
+    }
+    acc[VA - 1] = lacc;
   }
 
-  // Phase B: weighted covariances for i-chunk ch (fastfca.py:352-358); with REC
-  // also the likelihood at (P, v', lambda') (after-EM evaluation).
+  // Phase B: weighted covariances (fastfca.py:352-358), I <= 4 (all i in one
+  // pass); with REC also the likelihood at (P, v', lambda') (after-EM).
+  // Off-diagonal outer-product entries y_x conj(y_y) are (re, im) pairs and
+  // the diagonal |y_x|^2 terms are paired up, so every accumulation is FFMA2.
   template <bool REC>
   __device__ __forceinline__ void phaseB(R (&acc)[NB + 1], int ch) const {
+    using P2 = C2;
+    constexpr int NCXs = I * (I - 1) / 2;  // complex entries
+    constexpr int DP = I / 2;              // diagonal pairs
+    constexpr bool IODD = (I & 1) != 0;
+    (void)ch;
     const C2* yp = ys + rec0 * RS;
     const R* vp = vs + rec0 * JS;
+    P2 ac[I][NCXs > 0 ? NCXs : 1];
+    P2 ad[I][DP > 0 ? DP : 1];
+    R as[I];
+    R lacc = R(0);
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      as[i] = R(0);
+#pragma unroll
+      for (int c = 0; c < (NCXs > 0 ? NCXs : 1); ++c) ac[i][c] = mk<C2, R>(R(0), R(0));
+#pragma unroll
+      for (int c = 0; c < (DP > 0 ? DP : 1); ++c) ad[i][c] = mk<C2, R>(R(0), R(0));
+    }
 #pragma unroll 1
     for (int k = 0; k < npts; ++k, yp += rstep * RS, vp += rstep * JS) {
       C2 yv[I];
       R vj[JM], w[I];
       load_point(yp, vp, yv, vj);
       weights(vj, w);
+      R iw[I];
+#pragma unroll
+      for (int i = 0; i < I; ++i) iw[i] = rcp(w[i]);
       if constexpr (REC) {
         R q[I];
         transform_q(yv, q);
-        R l = R(0);
 #pragma unroll
-        for (int i = 0; i < I; ++i) l += flog(w[i]) + q[i] * rcp(w[i]);
-        acc[NB] += l;
+        for (int i = 0; i < I; ++i) lacc += flog(w[i]) + q[i] * iw[i];
       }
-      // lower-triangle outer product: per row x: diag, then (x, y<x) re, im
-      R O[I * I];
+      R dg[I];
+#pragma unroll
+      for (int x = 0; x < I; ++x) dg[x] = yv[x].x * yv[x].x + yv[x].y * yv[x].y;
+      P2 oc[NCXs > 0 ? NCXs : 1];
       {
-        int kk = 0;
+        int c = 0;
 #pragma unroll
-        for (int x = 0; x < I; ++x) {
-          O[kk++] = yv[x].x * yv[x].x + yv[x].y * yv[x].y;
+        for (int x = 1; x < I; ++x)
 #pragma unroll
-          for (int y2 = 0; y2 < x; ++y2) {
-            O[kk++] = yv[x].x * yv[y2].x + yv[x].y * yv[y2].y;
-            O[kk++] = yv[x].y * yv[y2].x - yv[x].x * yv[y2].y;
+          for (int y2 = 0; y2 < x; ++y2, ++c) {  // y_x conj(y_y) = y_y.x (y_x) + y_y.y (y_x.y, -y_x.x)
+            P2 t = fma2(yv[x], bc2<R>(yv[y2].x), mk<C2, R>(R(0), R(0)));
+            oc[c] = fma2(mk<C2, R>(yv[x].y, -yv[x].x), bc2<R>(yv[y2].y), t);
           }
-        }
       }
 #pragma unroll
-      for (int ii = 0; ii < IC; ++ii) {
-        const int i = ch * IC + ii;
-        if (i < I) {
-          const R iwv = rcp(w[i]);
+      for (int i = 0; i < I; ++i) {
+        const P2 b = bc2<R>(iw[i]);
 #pragma unroll
-          for (int kk = 0; kk < I * I; ++kk) acc[ii * I * I + kk] = fma(O[kk], iwv, acc[ii * I * I + kk]);
-        }
+        for (int c = 0; c < NCXs; ++c) ac[i][c] = fma2(oc[c], b, ac[i][c]);
+#pragma unroll
+        for (int c = 0; c < DP; ++c) ad[i][c] = fma2(mk<C2, R>(dg[2 * c], dg[2 * c + 1]), b, ad[i][c]);
+        if constexpr (IODD) as[i] = fma(dg[I - 1], iw[i], as[i]);
       }
     }
+    // flatten into the packed lower-triangle order: per row x, diag then (x, y<x)
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      R* o = acc + i * I * I;
+#pragma unroll
+      for (int x = 0; x < I; ++x) {
+        if (IODD && x == I - 1) o[x * x] = as[i];
+        else o[x * x] = (x & 1) ? ad[i][x / 2].y : ad[i][x / 2].x;
+      }
+      int c = 0;
+#pragma unroll
+      for (int x = 1; x < I; ++x)
+#pragma unroll
+        for (int y2 = 0; y2 < x; ++y2, ++c) {
+          o[x * x + 1 + 2 * y2] = ac[i][c].x;
+          o[x * x + 2 + 2 * y2] = ac[i][c].y;
+        }
+    }
+    acc[NB] = lacc;
   }
 
   // Phase B for I > 4: lanes with the same (bin g, group q) cooperate on one
