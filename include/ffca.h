@@ -180,6 +180,20 @@ int ffca_fca_mstep(int device, void* stream, int mem, int dtype, int U, int I, i
 int ffca_power_floor(int device, void* stream, int mem, int dtype, int U, int I, int N, int F, const void* y,
                      double* out);
 
+/* S_j = P^-H diag(lam_j) P^-1 hermitized, (U,J,F,I,I): fastfca.reconstruct_spatial_covariances
+ * (fastfca.py:119-135). */
+int ffca_reconstruct_covariances(int device, void* stream, int mem, int dtype, int U, int I, int J, int F,
+                                 const void* P, const void* lam, void* S, int* status);
+
+/* Posterior covariances in the microphone basis, P^-H diag(phi_t) P^-1 hermitized, (U,J,N,F,I,I):
+ * the phi half of fastfca.back_transform_stats (fastfca.py:276-287). */
+int ffca_back_transform_phi(int device, void* stream, int mem, int dtype, int U, int I, int J, int N, int F,
+                            const void* P, const void* phi_t, void* phi_out, int* status);
+
+/* Whitening init fastfca.params_from_covariances (fastfca.py:290-309): P (U,F,I,I), lam (U,J,F,I). */
+int ffca_params_from_covariances(int device, void* stream, int mem, int dtype, int U, int I, int J, int F,
+                                 const void* S_hat, void* P_out, void* lam_out, int* status);
+
 /* Launch plan of the loop kernel for a shape: out6 = {G, C, NL, threads, resident, smem}. */
 int ffca_plan_loop(int device, int dtype, int U, int I, int J, int N, int F, int vf_mode, int* out6);
 

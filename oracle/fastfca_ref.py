@@ -266,3 +266,24 @@ def run_fastfca(y, P0, lam0, v0, iterations=20, inner_iterations=1, v_floor=None
 def stats_refresh(P, lam, v, y):
     """Final transformed stats, (J,N,F,I) each.  fastfca.py:373-387."""
     return e_step_diag(P, lam, v, transform(P, y))
+
+
+def back_transform_stats(P, mu_t, phi_t):
+    """(mu (J,N,F,I), phi (J,N,F,I,I)) in the microphone basis.  fastfca.py:276-287."""
+    mu = back_transform_means(P, mu_t)
+    A = np.linalg.inv(np.conj(np.swapaxes(P, -1, -2)))
+    phi = np.einsum("fai,jnfi,fbi->jnfab", A, phi_t, np.conj(A))
+    return mu, hermitize(phi)
+
+
+def params_from_covariances(S_hat, v):
+    """Whitening init: P = (chol(sum_j S_j)^H)^-1, lam = diag(P^H S_j P).  fastfca.py:290-309."""
+    total = S_hat.sum(axis=0)
+    try:
+        low = np.linalg.cholesky(total)
+    except np.linalg.LinAlgError as exc:
+        raise OracleSingular("NotPositiveDefinite", str(exc)) from exc
+    P = np.linalg.inv(np.conj(np.swapaxes(low, -1, -2)))
+    lam = np.real(np.einsum("fai,jfab,fbi->jfi", np.conj(P), S_hat, P))
+    lam = np.maximum(lam, LAMBDA_FLOOR_RTOL * lam.max(axis=-1, keepdims=True))
+    return P, lam, np.asarray(v, dtype=np.float64)

@@ -393,3 +393,50 @@ def images_from_state(obs: ObservationTensor, params: FastFcaParams) -> np.ndarr
                                        _lib.ptr(_as_r(params.Lam, c64)), _lib.ptr(_as_r(params.v, c64)),
                                        _lib.ptr(out), None), "ffca_fastfca_images")
     return out
+
+
+def back_transform_stats(params: FastFcaParams, stats: TransformedStats):
+    """(mu (J,N,F,I), phi (J,N,F,I,I)) in the microphone basis.  fastfca.py:276-287."""
+    lib = _lib.require_gpu()
+    c64 = params.P.dtype == np.complex64
+    mu = back_transform_means(params.P, stats.mu)
+    phi_t = _as_r(stats.phi, c64)
+    J, N, F, I = phi_t.shape
+    out = np.empty((J, N, F, I, I), np.complex64 if c64 else np.complex128)
+    _lib.check(lib.ffca_back_transform_phi(_lib.device(), None, _lib.MEM_HOST, _code(c64), 1, I, J, N, F,
+                                           _lib.ptr(_as_c(params.P, c64)), _lib.ptr(phi_t), _lib.ptr(out), None),
+               "ffca_back_transform_phi")
+    return mu, out
+
+
+def reconstruct_spatial_covariances(params: FastFcaParams) -> np.ndarray:
+    """All S_j(f) = P^{-H} Lambda_j P^{-1}, (J, F, I, I), hermitized.  fastfca.py:119-126."""
+    lib = _lib.require_gpu()
+    c64 = params.P.dtype == np.complex64
+    J, F, I = params.Lam.shape
+    S = np.empty((J, F, I, I), params.P.dtype)
+    _lib.check(lib.ffca_reconstruct_covariances(_lib.device(), None, _lib.MEM_HOST, _code(c64), 1, I, J, F,
+                                                _lib.ptr(params.P), _lib.ptr(params.Lam), _lib.ptr(S), None),
+               "ffca_reconstruct_covariances")
+    return S
+
+
+def reconstruct_spatial_covariance(params: FastFcaParams, j: int, f: int) -> np.ndarray:
+    """S_j(f) for one source and bin.  fastfca.py:129-135."""
+    one = FastFcaParams(P=params.P[f:f + 1], Lam=params.Lam[j:j + 1, f:f + 1], v=params.v[j:j + 1, :, f:f + 1])
+    return reconstruct_spatial_covariances(one)[0, 0]
+
+
+def params_from_covariances(S_hat: np.ndarray, v: np.ndarray) -> FastFcaParams:
+    """Whitening initialization from spatial covariance estimates.  fastfca.py:290-309."""
+    lib = _lib.require_gpu()
+    S_hat = np.asarray(S_hat)
+    c64 = S_hat.dtype == np.complex64
+    S_hat = _as_c(S_hat, c64)
+    J, F, I, _ = S_hat.shape
+    P = np.empty((F, I, I), S_hat.dtype)
+    lam = np.empty((J, F, I), np.float32 if c64 else np.float64)
+    _lib.check(lib.ffca_params_from_covariances(_lib.device(), None, _lib.MEM_HOST, _code(c64), 1, I, J, F,
+                                                _lib.ptr(S_hat), _lib.ptr(P), _lib.ptr(lam), None),
+               "ffca_params_from_covariances")
+    return FastFcaParams(P=P, Lam=lam, v=_as_r(v, c64))

@@ -94,6 +94,20 @@ def main():
         "step/one_iter_P": fastfca.run_fastfca(obs, params, iterations=1, v_floor=0.0).params.P,
     })
 
+    # --- back-transformed stats, reconstruction, whitening init
+    mu_b, phi_b = fastfca.back_transform_stats(params, st)
+    rngw = np.random.default_rng(9)
+    a = rngw.standard_normal((3, 5, 3, 3)) + 1j * rngw.standard_normal((3, 5, 3, 3))
+    S_hat = a @ np.conj(np.swapaxes(a, -1, -2)) + np.eye(3)
+    S_hat = 0.5 * (S_hat + np.conj(np.swapaxes(S_hat, -1, -2)))
+    v_hat = rngw.uniform(0.5, 2.0, (3, 7, 5))
+    init = fastfca.params_from_covariances(S_hat, v_hat)
+    out.update({
+        "init/S_hat": S_hat, "init/v_hat": v_hat, "init/P": init.P, "init/Lam": init.Lam,
+        "step/bt_mu": mu_b, "step/bt_phi": phi_b,
+        "step/S01": fastfca.reconstruct_spatial_covariance(params, 1, 2),
+    })
+
     # --- conventional FCA
     I, J, F, N = 3, 3, 6, 24
     y, P0, lam0, v0, _ = mixture(21, I, J, F, N)

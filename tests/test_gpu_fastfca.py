@@ -340,3 +340,40 @@ def test_pipelined_host_call_is_bitwise_one_launch(shape):
         os.environ.pop("FFCA_PIPELINE_MIN_BYTES")
     for a, b in zip(got, ref):
         assert np.array_equal(a, b)
+
+
+def test_back_transform_stats_reconstruct_and_init_golden(golden):
+    g = case(golden, "step")
+    params = fastfca.FastFcaParams(g["P"], g["lam"], g["v"])
+    st = fastfca.e_step_diag(params, fastfca.transform_observations(g["P"], ObservationTensor(g["y"])))
+    mu, phi = fastfca.back_transform_stats(params, st)
+    assert rel(mu, g["bt_mu"]) <= 1e-12 and rel(phi, g["bt_phi"]) <= 1e-12
+    assert rel(fastfca.reconstruct_spatial_covariances(params), g["S"]) <= 1e-12
+    assert rel(fastfca.reconstruct_spatial_covariance(params, 1, 2), g["S01"]) <= 1e-12
+    h = case(golden, "init")
+    init = fastfca.params_from_covariances(h["S_hat"], h["v_hat"])
+    assert rel(init.P, h["P"]) <= 1e-12 and rel(init.Lam, h["Lam"]) <= 1e-12
+    with pytest.raises(errors.NotPositiveDefinite):
+        fastfca.params_from_covariances(-h["S_hat"], h["v_hat"])
+
+
+def test_equivalence_to_full_fca_estep(rng):
+    # acceptance criterion 2 (test_acceptance.py:132-176): the back-transformed
+    # diagonal-path E-step equals the full-matrix E-step on the reconstructed S
+    from paper_1805_09498_b200 import fca
+    worst = 0.0
+    for order in (2, 3, 4):
+        for trial in range(6):
+            r = np.random.default_rng(1000 * order + trial)
+            P = r.standard_normal((4, order, order)) + 1j * r.standard_normal((4, order, order)) + 2 * np.eye(order)
+            params = fastfca.FastFcaParams(P, r.uniform(0.5, 2.0, (order, 4, order)),
+                                           r.uniform(0.5, 2.0, (order, 8, 4)))
+            obs = ObservationTensor(r.standard_normal((order, 8, 4)) + 1j * r.standard_normal((order, 8, 4)))
+            st = fastfca.e_step_diag(params, fastfca.transform_observations(P, obs))
+            mu, phi = fastfca.back_transform_stats(params, st)
+            full = fca.FcaParams(S=fastfca.reconstruct_spatial_covariances(params), v=params.v)
+            ref = fca.e_step(full, obs)
+            worst = max(worst, np.abs(mu - ref.mu).max(), np.abs(phi - ref.phi).max())
+            l1, l2 = fca.log_likelihood(full, obs), fastfca.log_likelihood(params, obs)
+            assert abs(l2 - l1) <= 1e-8 * abs(l1)
+    assert worst <= 1e-8

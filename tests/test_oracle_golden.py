@@ -61,6 +61,17 @@ def test_unfused_steps(golden):
     assert rel(one.P, g["one_iter_P"]) <= 1e-12
 
 
+def test_back_transform_stats_and_init(golden):
+    g = {k.split("/", 1)[1]: v for k, v in golden.items() if k.startswith("step/")}
+    mu, phi = ffr.e_step_diag(g["P"], g["lam"], g["v"], ffr.transform(g["P"], g["y"]))
+    bmu, bphi = ffr.back_transform_stats(g["P"], mu, phi)
+    assert rel(bmu, g["bt_mu"]) <= 1e-12 and rel(bphi, g["bt_phi"]) <= 1e-12
+    assert rel(ffr.reconstruct_spatial_covariances(g["P"], g["lam"])[1, 2], g["S01"]) <= 1e-12
+    h = {k.split("/", 1)[1]: v for k, v in golden.items() if k.startswith("init/")}
+    P, lam, _ = ffr.params_from_covariances(h["S_hat"], h["v_hat"])
+    assert rel(P, h["P"]) <= 1e-12 and rel(lam, h["Lam"]) <= 1e-12
+
+
 def test_fca_baseline(golden):
     g = {k.split("/", 1)[1]: v for k, v in golden.items() if k.startswith("fca/")}
     run = fca_ref.run_fca(g["y"], g["S0"], g["v0"], iterations=int(g["iters"]), record_likelihood=True)
