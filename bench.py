@@ -181,9 +181,9 @@ def run_ours(args, rank, world, local_rank):
     u0 = total * rank // world
     u1 = total * (rank + 1) // world
     U = u1 - u0
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", local_rank % max(1, torch.cuda.device_count()))
     torch.cuda.set_device(dev)
-    _lib.set_device(local_rank)
+    _lib.set_device(dev.index)
     lib = _lib.require_gpu()
     code = _lib.C64 if cfg.dtype == "c64" else _lib.C128
     I, J, N, F, T = cfg.I, cfg.J, cfg.N, cfg.F, cfg.iterations
@@ -197,7 +197,7 @@ def run_ours(args, rank, world, local_rank):
     sptr = stream.cuda_stream
 
     def step():
-        rc = lib.ffca_fastfca_run(local_rank, sptr, _lib.MEM_DEVICE, code, U, I, J, N, F, y.data_ptr(),
+        rc = lib.ffca_fastfca_run(dev.index, sptr, _lib.MEM_DEVICE, code, U, I, J, N, F, y.data_ptr(),
                                   P0.data_ptr(), lam0.data_ptr(), v0.data_ptr(), _lib.VF_AUTO, 0.0, None, T, 1,
                                   0, P.data_ptr(), lam.data_ptr(), v.data_ptr(), None, None, None)
         _lib.check(rc, "ffca_fastfca_run")
@@ -208,7 +208,7 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(dev.index)
     time.sleep(0.3)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -224,7 +224,8 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     elapsed_ms = ev0.elapsed_time(ev1)
-    t_ms = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    tdev = dev if dist.is_initialized() and dist.get_backend() == "nccl" else "cpu"
+    t_ms = torch.tensor([elapsed_ms], dtype=torch.float64, device=tdev)
     if world > 1:
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
     ms_per_step = float(t_ms.item()) / args.steps
@@ -238,10 +239,11 @@ def run_ours(args, rank, world, local_rank):
         g0 = torch.cuda.Event(enable_timing=True)
         g1 = torch.cuda.Event(enable_timing=True)
         g0.record(stream)
-        shards = [torch.empty_like(P) for _ in range(world)] if rank == 0 else None
-        # equal-size shards are required by gather; pad by re-sending when uneven
+        src = torch.view_as_real(P if tdev != "cpu" else P.cpu()).contiguous()
+        shards = [torch.empty_like(src) for _ in range(world)] if rank == 0 else None
+        # equal-size shards are required by gather (256 mixtures split evenly for N | 256)
         if all((total * (r + 1) // world - total * r // world) == U for r in range(world)):
-            dist.gather(P, shards, dst=0)
+            dist.gather(src, shards, dst=0)
         g1.record(stream)
         torch.cuda.synchronize()
         gather_ms = g0.elapsed_time(g1)
@@ -255,10 +257,12 @@ def run_ours(args, rank, world, local_rank):
     achieved = algo_bytes_pt * units_launch / (k_ms / 1e3) / 1e9
     peak, peak_src = peak_hbm()
     tr = ncu_traffic()
+    if tr and tr.get("units_per_launch") not in (None, units_launch):
+        tr = None  # the committed capture is for a different launch size
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4),
                 "traffic": (tr or {}).get("dram_bytes_per_launch"),
-                "kernel": "ffca_loop_kernel<float,3,3,true>",
+                "kernel": "ffca_loop_kernel<float,3,3,4,true>",
                 "kernel_ms": round(k_ms, 4),
                 "algorithmic_bytes_per_unit": algo_bytes_pt,
                 "units_per_launch": units_launch,
@@ -295,7 +299,7 @@ def run_ours(args, rank, world, local_rank):
             api_step()
         e1.record(stream)
         torch.cuda.synchronize()
-        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=tdev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_ms = float(te.item()) / args.steps
@@ -392,8 +396,14 @@ def main():
     import torch
     import torch.distributed as dist
     if world > 1:
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        ndev = max(1, torch.cuda.device_count())
+        torch.cuda.set_device(local_rank % ndev)
+        # FFCA_DIST_BACKEND=gloo lets the multi-rank path be exercised with several ranks per GPU
+        backend = os.environ.get("FFCA_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank % ndev))
+        else:
+            dist.init_process_group(backend)
     try:
         run_ours(args, rank, world, local_rank)
     finally:

@@ -377,3 +377,56 @@ def test_equivalence_to_full_fca_estep(rng):
             l1, l2 = fca.log_likelihood(full, obs), fastfca.log_likelihood(params, obs)
             assert abs(l2 - l1) <= 1e-8 * abs(l1)
     assert worst <= 1e-8
+
+
+def _model_observation(rng, params):
+    """y ~ CN(0, sum_j v_j S_j) from the jointly diagonalized model (test_fastfca.py:23-36 pattern)."""
+    J, N, F = params.v.shape
+    S = fastfca.reconstruct_spatial_covariances(params)
+    chol = np.linalg.cholesky(S)
+    y = np.zeros((N, F, params.order), dtype=complex)
+    for j in range(J):
+        z = (rng.standard_normal((N, F, params.order)) + 1j * rng.standard_normal((N, F, params.order))) / np.sqrt(2)
+        y += np.sqrt(params.v[j])[..., None] * np.einsum("fab,nfb->nfa", chol[j], z)
+    return ObservationTensor(y.transpose(2, 0, 1))
+
+
+def _rand_params(rng, J, N, F, I):
+    P = rng.standard_normal((F, I, I)) + 1j * rng.standard_normal((F, I, I)) + 2.0 * np.eye(I)
+    return fastfca.FastFcaParams(P, rng.uniform(0.5, 1.5, (J, F, I)), rng.uniform(0.5, 1.5, (J, N, F)))
+
+
+def test_em_substep_monotone_and_likelihood_improves(rng):
+    # test_fastfca.py:369-386 and acceptance criterion 3
+    truth = _rand_params(rng, 3, 48, 4, 3)
+    obs = _model_observation(rng, truth)
+    init = _rand_params(rng, 3, 48, 4, 3)
+    run = fastfca.run_fastfca(obs, init, iterations=15, record_likelihood=True)
+    before = [run.loglik_init] + run.loglik_after_p[:-1]
+    for prev, new in zip(before, run.loglik_after_em):
+        assert new >= prev - 1e-6 * abs(prev)
+    assert run.loglik_after_p[-1] > run.loglik_init
+
+
+def test_fixed_point_stationarity_after_convergence():
+    # acceptance criterion 7 (test_acceptance.py:255-295): after 150 iterations
+    # one more fixed-point update moves the columns of P by <= 1e-6
+    r = np.random.default_rng(77)
+    I, J, N, F = 3, 1, 512, 4
+    P_true = r.standard_normal((F, I, I)) + 1j * r.standard_normal((F, I, I)) + 2 * np.eye(I)
+    truth = fastfca.FastFcaParams(P_true, r.uniform(0.5, 3.0, (J, F, I)), r.uniform(0.3, 3.0, (J, N, F)))
+    obs = _model_observation(r, truth)
+    init = fastfca.FastFcaParams(P_true + 0.2 * (r.standard_normal(P_true.shape) + 1j * r.standard_normal(P_true.shape)),
+                                 truth.Lam * r.uniform(0.7, 1.4, truth.Lam.shape),
+                                 truth.v * r.uniform(0.7, 1.4, truth.v.shape))
+    run = fastfca.run_fastfca(obs, init, iterations=150)
+    upd = fastfca.fixed_point_update_P(run.params, obs)
+    resid = (np.linalg.norm(upd - run.params.P, axis=1) / np.linalg.norm(run.params.P, axis=1)).max()
+    assert resid <= 1e-6
+
+
+def test_counters_match_paper_at_benchmark_size():
+    # acceptance criterion 1: I=3, F=512 -> exactly 2048 inversions per iteration, 0 matmuls
+    y, P0, lam0, v0, _ = mixture(1, 3, 3, 512, 8)
+    run = fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=1)
+    assert run.counters.inversions == 2048 and run.counters.matmuls == 0
