@@ -42,7 +42,9 @@ static int choose_threads(int G, int NL, int I) {
   t = (t + 31) / 32 * 32;
   const int tmin = I > 4 ? (8 * (I + 1) + 31) / 32 * 32 : 64;  // I > 4: 8-lane solver groups
   if (t < tmin) t = tmin;
-  if (t > 256) t = 256;
+  // I >= 4 instantiations use up to 255 registers: 128-thread CTAs keep two per SM
+  const int tmax = I >= 4 ? 128 : 256;
+  if (t > tmax) t = tmax;
   return t;
 }
 
