@@ -231,6 +231,7 @@ struct SmallLU {
   bool ok;
   double logabsdet;
 
+  template <bool LOGDET = true>
   __device__ __forceinline__ void factor() {
     ok = true;
     logabsdet = 0.0;
@@ -257,7 +258,7 @@ struct SmallLU {
       const double2 d = a[k][k];
       if (d.x == 0.0 && d.y == 0.0) ok = false;
       rd[k] = crecip(d);
-      logabsdet += log(hypot(d.x, d.y));
+      if (LOGDET) logabsdet += log(hypot(d.x, d.y));
 #pragma unroll
       for (int r = k + 1; r < I; ++r) {
         const double2 l = cmul(a[r][k], rd[k]);

@@ -165,16 +165,43 @@ __device__ __forceinline__ void bin_reduce_tail(int nv, double* wpart, double* c
   __syncthreads();
 }
 
+// One level of the halving butterfly (offset O, M live values), recursing to O/2.
+template <typename R, int M, int O, int G, int N>
+__device__ __forceinline__ void halving_step(R (&buf)[N], int lane, int& base) {
+  if constexpr (O >= G) {
+    const bool hi = (lane & O) != 0;
+#pragma unroll
+    for (int k = 0; k < M / 2; ++k) {
+      const R keep = hi ? buf[k + M / 2] : buf[k];
+      const R send = hi ? buf[k] : buf[k + M / 2];
+      buf[k] = keep + __shfl_xor_sync(FULL, send, O);
+    }
+    if (hi) base += M / 2;
+    halving_step<R, M / 2, O / 2, G>(buf, lane, base);
+  }
+}
+
+// Warp half of the reduction as a transposed (halving) butterfly over the
+// L = 32/G lanes of a bin: at each step a lane keeps one half of its current
+// values and receives the partner's copy of that half, so the V values take
+// ~V shuffles instead of V*log2(L).  Lane with in-bin bits (b16..bG) ends up
+// owning values [base, base + V2/L), base = sum_s b_s * V2 / 2^(s+1).
 template <typename R, int V, int G>
 __device__ __forceinline__ void bin_reduce(const R (&vals)[V], double* wpart, double* cpart, double* tot, int C,
                                            int VMAX, int& parity) {
+  constexpr int L = 32 / G;
+  constexpr int V2 = (V + L - 1) / L * L;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane % G;
+  R buf[V2];
 #pragma unroll
-  for (int k = 0; k < V; ++k) {
-    const R s = bin_warp_sum<G>(vals[k]);
-    if (lane < G) wpart[(warp * G + g) * VMAX + k] = double(s);
-  }
+  for (int k = 0; k < V2; ++k) buf[k] = k < V ? vals[k] : R(0);
+  int base = 0;
+  halving_step<R, V2, 16, G>(buf, lane, base);
+  double* row = wpart + (warp * G + g) * VMAX;
+#pragma unroll
+  for (int k = 0; k < V2 / L; ++k)
+    if (base + k < V) row[base + k] = double(buf[k]);
   bin_reduce_tail<G>(V, wpart, cpart, tot, C, VMAX, parity);
 }
 
@@ -834,9 +861,10 @@ __global__ void __launch_bounds__(256, (I > 3 ? 1 : 2)) ffca_loop_kernel(const L
           for (int x = 0; x < I; ++x)
 #pragma unroll
             for (int y2 = 0; y2 < I; ++y2) lu.a[x][y2] = Pd[(gg * I + x) * I + y2];
-          lu.factor();
+          if (rec && k == 0) lu.template factor<true>();
+          else lu.template factor<false>();
           if (!lu.ok && crank == 0) atomicOr(&a.status[b], ST_SINGULAR_P);
-          if (k == 0) ldet[gg] = lu.logabsdet;
+          if (rec && k == 0) ldet[gg] = lu.logabsdet;
 #pragma unroll
           for (int x = 0; x < I; ++x) {
 #pragma unroll
