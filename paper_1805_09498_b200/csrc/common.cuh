@@ -131,7 +131,7 @@ __device__ __forceinline__ double2 crecip(const double2 z) {
   // [2^-500, 2^500] so |z|^2 neither overflows nor underflows.
   const double m = fmax(fabs(z.x), fabs(z.y));
   if (m > 0x1p-500 && m < 0x1p500) {
-    const double r = 1.0 / (z.x * z.x + z.y * z.y);
+    const double r = rcp(z.x * z.x + z.y * z.y);
     return make_double2(z.x * r, -z.y * r);
   }
   const int e = ilogb(m);
@@ -332,7 +332,7 @@ struct SmallLDL {
       for (int c = 0; c < k; ++c) dk -= (l[k][c].x * l[k][c].x + l[k][c].y * l[k][c].y) * d[c];
       d[k] = dk;
       if (dk == 0.0) ok = false;
-      rd[k] = 1.0 / dk;
+      rd[k] = (dk != 0.0) ? rcp(dk) : 0.0;
 #pragma unroll
       for (int r = k + 1; r < I; ++r) {
         double2 acc = b[r][k];

@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(256) fca_estep_kernel(const FcaEstepArgs a) {
     for (int c = 0; c < k; ++c) dk -= (L[k][c].x * L[k][c].x + L[k][c].y * L[k][c].y) * d[c];
     d[k] = dk;
     bad = bad || dk == R(0);
-    rd[k] = R(1) / dk;
+    rd[k] = rcp(dk);
 #pragma unroll
     for (int r = k + 1; r < I; ++r) {
       C2 acc = L[r][k];

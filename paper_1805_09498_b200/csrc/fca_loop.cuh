@@ -166,7 +166,7 @@ struct FcaPoint {
         for (int c = 0; c < kk; ++c) dk -= (L[kk][c].x * L[kk][c].x + L[kk][c].y * L[kk][c].y) * d[c];
         d[kk] = dk;
         if (dk == R(0)) bad = 1;
-        rd[kk] = R(1) / dk;
+        rd[kk] = rcp(dk);
 #pragma unroll
         for (int r = kk + 1; r < I; ++r) {
           C2 acc2 = L[r][kk];
@@ -283,7 +283,7 @@ struct FcaPoint {
         if constexpr (VF2) fl = fp[j];
         const R vn = fmax(tr * invI, fl);
         wp[j] = vn;
-        const R iv = R(1) / vn;
+        const R iv = rcp(vn);
 #pragma unroll
         for (int e = 0; e < H; ++e) acc[j * H + e] = fma(Tl[e], iv, acc[j * H + e]);
       }
@@ -330,7 +330,7 @@ struct FcaPoint {
         for (int c = 0; c < kk; ++c) dk -= (L[kk][c].x * L[kk][c].x + L[kk][c].y * L[kk][c].y) * d[c];
         d[kk] = dk;
         if (dk == R(0)) bad = 1;
-        rd[kk] = R(1) / dk;
+        rd[kk] = rcp(dk);
 #pragma unroll
         for (int r = kk + 1; r < I; ++r) {
           C2 acc2 = L[r][kk];
