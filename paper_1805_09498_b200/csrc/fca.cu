@@ -39,7 +39,12 @@ static int plan_fca(int dtype, int I, int J, int N, int vf_mode, FcaPlan& p, siz
     p.C = C;
     p.NL = (N + C - 1) / C;
     int t = ((p.NL + 3) / 4 + 31) / 32 * 32;
-    p.threads = t < 64 ? 64 : (t > 256 ? 256 : t);
+    // 255-register instantiations: 128-thread CTAs keep two resident per SM
+    p.threads = t < 64 ? 64 : (t > 128 ? 128 : t);
+    if (const char* ft = getenv("FFCA_FCA_THREADS")) {  // tuning hook
+      const int v = atoi(ft);
+      if (v >= 64 && v <= 256 && v % 32 == 0) p.threads = v;
+    }
     FcaSmem L(I, J, p.NL, p.threads / 32, rsz, vf_mode, VMAX);
     p.smem = L.total;
     if (L.slab <= 100 * 1024 && p.smem <= optin) return FFCA_OK;
