@@ -318,7 +318,7 @@ struct PointWork {
       P2 Q[I];
 #pragma unroll
       for (int i = 0; i < I; ++i) {
-        const R iw = rcp(w[i]);
+        const R iw = rcp_pt(w[i]);
         Q[i] = mk<C2, R>(iw, (q[i] * iw) * iw);
       }
       if constexpr (REC) {
@@ -339,7 +339,7 @@ struct PointWork {
           R fl = vfl_b;
           if constexpr (VF2) fl = fp[j];
           const R vn = fmax(v - step, fl);
-          const R ratio = v * rcp(vn);
+          const R ratio = v * rcp_pt(vn);
           s0[j] += ratio;
           const R rv = ratio * v;
 #pragma unroll
@@ -395,7 +395,7 @@ struct PointWork {
       weights(vj, w);
       R iw[I];
 #pragma unroll
-      for (int i = 0; i < I; ++i) iw[i] = rcp(w[i]);
+      for (int i = 0; i < I; ++i) iw[i] = rcp_pt(w[i]);
       if constexpr (REC) {
         R q[I];
         transform_q(yv, q);
@@ -477,7 +477,7 @@ struct PointWork {
 #pragma unroll
         for (int j = 0; j < JM; ++j)
           if (j < J) s = fma(vp[j], Lam(j, p), s);
-        iw_own = rcp(fmax(s, wfl));
+        iw_own = rcp_pt(fmax(s, wfl));
       }
       R iw[I];
 #pragma unroll
@@ -528,7 +528,7 @@ struct PointWork {
       transform_q(yv, q);
       weights(vj, w);
 #pragma unroll
-      for (int i = 0; i < I; ++i) acc[0] += flog(w[i]) + q[i] * rcp(w[i]);
+      for (int i = 0; i < I; ++i) acc[0] += flog(w[i]) + q[i] * rcp_pt(w[i]);
     }
   }
 };
