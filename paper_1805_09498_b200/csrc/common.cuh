@@ -107,6 +107,13 @@ __device__ __forceinline__ void cmac_conj(C2& acc, const C2 p, const C2 y) {
   acc.y = fma(p.x, y.y, fma(-p.y, y.x, acc.y));
 }
 
+// Dynamic shared memory actually granted to this launch (bytes).
+__device__ __forceinline__ unsigned dynamic_smem_bytes() {
+  unsigned r;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+  return r;
+}
+
 // Asynchronous global -> shared copy of one element (cp.async, LDGSTS);
 // `valid == false` zero-fills the destination without reading the source.
 template <int BYTES>

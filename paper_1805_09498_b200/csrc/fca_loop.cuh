@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(256) fca_loop_kernel(const FcaArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int W = blockDim.x >> 5;
   const FcaSmem L(I, J, a.NL, W, sizeof(R), a.vf_mode, VMAX);
+  if (L.total > dynamic_smem_bytes()) __trap();
   int crank = 0;
   if (C > 1) crank = int(cg::this_cluster().block_rank());
   int parity = 0;

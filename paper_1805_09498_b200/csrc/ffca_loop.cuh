@@ -553,6 +553,8 @@ __global__ void __launch_bounds__(256, (I > 3 ? 1 : 2)) ffca_loop_kernel(const L
   const int W = blockDim.x >> 5;
   const bool resident = RES || a.scratch == nullptr;
   const LoopSmem L(I, J, G, a.NL, W, sizeof(R), a.vf_mode, resident, VMAX);
+  // the host sized the launch with the same carve-up; trap rather than run past it
+  if (L.total > dynamic_smem_bytes()) __trap();
 
   int crank = 0;
   if (C > 1) crank = int(cg::this_cluster().block_rank());
