@@ -464,6 +464,19 @@ struct PointWork {
     // warp-uniform trip count (every lane must reach the shuffles); lanes whose
     // point is out of range, or whose bin is padding, contribute nothing
     const int trips = (NLr > warp * QW) ? (NLr - warp * QW + stride - 1) / stride : 0;
+    // pair accumulators: (re, im) of each owned complex entry per i (FFMA2)
+    C2 ac[NSL ? NSL : 1][I];
+    R ad[I];
+    R lacc = R(0);
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      ad[i] = R(0);
+#pragma unroll
+      for (int s = 0; s < (NSL ? NSL : 1); ++s) ac[s][i] = mk<C2, R>(R(0), R(0));
+    }
+    bool own[NSL ? NSL : 1];
+#pragma unroll
+    for (int s = 0; s < NSL; ++s) own[s] = p + 8 * s < Shape<I>::NCX;
 #pragma unroll 1
     for (int k = 0; k < trips; ++k) {
       const int n = start + k * stride;
@@ -486,18 +499,16 @@ struct PointWork {
         const C2 yd = yp[p];
         const R dv = yd.x * yd.x + yd.y * yd.y;
 #pragma unroll
-        for (int i = 0; i < I; ++i) acc[i] = fma(dv, iw[i], acc[i]);
+        for (int i = 0; i < I; ++i) ad[i] = fma(dv, iw[i], ad[i]);
       }
 #pragma unroll
       for (int s = 0; s < NSL; ++s) {
-        if (valid && p + 8 * s < Shape<I>::NCX) {
+        if (valid && own[s]) {
           const C2 a = yp[cx[s]], b = yp[cy[s]];
-          const R re = a.x * b.x + a.y * b.y, im = a.y * b.x - a.x * b.y;
+          // a conj(b) = b.x (a.x, a.y) + b.y (a.y, -a.x)
+          const C2 o = fma2(mk<C2, R>(a.y, -a.x), bc2<R>(b.y), fma2(a, bc2<R>(b.x), mk<C2, R>(R(0), R(0))));
 #pragma unroll
-          for (int i = 0; i < I; ++i) {
-            acc[(1 + 2 * s) * I + i] = fma(re, iw[i], acc[(1 + 2 * s) * I + i]);
-            acc[(2 + 2 * s) * I + i] = fma(im, iw[i], acc[(2 + 2 * s) * I + i]);
-          }
+          for (int i = 0; i < I; ++i) ac[s][i] = fma2(o, bc2<R>(iw[i]), ac[s][i]);
         }
       }
       if constexpr (REC) {
@@ -510,10 +521,20 @@ struct PointWork {
           R l = R(0);
 #pragma unroll
           for (int i = 0; i < I; ++i) l += flog(R(1) / iw[i]) + q2[i] * iw[i];
-          acc[NVG - 1] += l;
+          lacc += l;
         }
       }
     }
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      acc[i] = ad[i];
+#pragma unroll
+      for (int s = 0; s < NSL; ++s) {
+        acc[(1 + 2 * s) * I + i] = ac[s][i].x;
+        acc[(2 + 2 * s) * I + i] = ac[s][i].y;
+      }
+    }
+    acc[NVG - 1] = lacc;
   }
 
   // Likelihood partial sum_n,i ln w + q / w at the current state.
