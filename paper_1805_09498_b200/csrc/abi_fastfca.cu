@@ -86,6 +86,16 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
     fill(G, 1, true);
     if (p.slab <= kSlabBudget && p.smem <= smem_optin) return FFCA_OK;
   }
+  // I > 4: the per-iteration reductions (I^3 values) and solves dominate a
+  // cluster's small per-CTA frame ranges; one 256-thread CTA per bin streaming
+  // its slab from L2-resident global scratch is faster (measured on config 4).
+  if (I > 4) {
+    fill(1, 1, false);
+    p.threads = 256;
+    LoopSmem L(I, J, 1, p.NL, 8, rsz, vf_mode, false, VMAX);
+    p.smem = L.total;
+    if (p.smem <= smem_optin) return FFCA_OK;
+  }
   for (int C = 2; C <= 8; C <<= 1) {
     if (C > N) break;
     fill(1, C, true);
