@@ -555,7 +555,7 @@ struct PointWork {
 };
 
 template <typename R, int I, int JT, int G, bool RES>
-__global__ void __launch_bounds__(256, (I > 3 ? 1 : 2)) ffca_loop_kernel(const LoopArgs a) {
+__global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const LoopArgs a) {
   using C2 = typename Cpx<R>::T;
   constexpr int JM = JT > 0 ? JT : 8;
   constexpr int IC = Shape<I>::IC, NCH = Shape<I>::NCH, NB = Shape<I>::NB;
