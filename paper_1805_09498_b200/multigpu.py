@@ -23,12 +23,13 @@ def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
     return total * rank // world, total * (rank + 1) // world
 
 
-def _device_compute(y, P0, lam0, v0, iterations, inner_iterations, v_floor):
+def _device_compute(y, P0, lam0, v0, iterations, inner_iterations, v_floor, record_likelihood=False):
     from .fastfca import run_fastfca_batch
 
-    P, lam, v, _ = run_fastfca_batch(y, P0, lam0, v0, iterations=iterations,
-                                     inner_iterations=inner_iterations, v_floor=v_floor)
-    return P, lam, v
+    P, lam, v, ll = run_fastfca_batch(y, P0, lam0, v0, iterations=iterations,
+                                      inner_iterations=inner_iterations, v_floor=v_floor,
+                                      record_likelihood=record_likelihood)
+    return (P, lam, v, ll) if record_likelihood else (P, lam, v)
 
 
 def _all_gather_concat(arr: np.ndarray, axis: int, group, world: int, device):
@@ -60,14 +61,18 @@ def _all_gather_concat(arr: np.ndarray, axis: int, group, world: int, device):
 
 
 def run_fastfca_sharded(y, P0, lam0, v0, iterations=20, inner_iterations=1, v_floor=None, mode="mixtures",
-                        group=None, compute=None, device=None):
+                        group=None, compute=None, device=None, record_likelihood=False):
     """Run the batched estimator with this rank's shard and all-gather the result.
 
     y (U, I, N, F), P0 (U, F, I, I), lam0 (U, J, F, I), v0 (U, J, N, F) are the
     full inputs on every rank (host numpy).  `compute` defaults to the device
     path (`fastfca.run_fastfca_batch`); it has the signature
-    compute(y, P0, lam0, v0, iterations, inner_iterations, v_floor) -> (P, lam, v).
-    Returns (P, lam, v) for all mixtures / bins on every rank.
+    compute(y, P0, lam0, v0, iterations, inner_iterations, v_floor[, record_likelihood])
+    -> (P, lam, v[, ll]).  Returns (P, lam, v) for all mixtures / bins on every
+    rank, plus the per-mixture log-likelihood history (U, 1+2T) when
+    ``record_likelihood``: concatenated over mixture shards, or summed over
+    F-block shards (each block's partial already carries its share of the
+    -N F I ln(pi) constant) with one all-reduce.
     """
     import torch.distributed as dist
 
@@ -80,18 +85,31 @@ def run_fastfca_sharded(y, P0, lam0, v0, iterations=20, inner_iterations=1, v_fl
     if mode == "mixtures":
         lo, hi = shard_range(U, rank, world)
         vf = v_floor if (v_floor is None or np.ndim(v_floor) == 0) else np.asarray(v_floor)[lo:hi]
-        P, lam, v = compute(y[lo:hi], P0[lo:hi], lam0[lo:hi], v0[lo:hi], iterations, inner_iterations, vf)
+        res = compute(y[lo:hi], P0[lo:hi], lam0[lo:hi], v0[lo:hi], iterations, inner_iterations, vf,
+                      *((True,) if record_likelihood else ()))
         axes = (0, 0, 0)
     elif mode == "bins":
         lo, hi = shard_range(F, rank, world)
         vf = v_floor if (v_floor is None or np.ndim(v_floor) == 0) else np.asarray(v_floor)[..., lo:hi]
-        P, lam, v = compute(np.ascontiguousarray(y[..., lo:hi]), np.ascontiguousarray(P0[:, lo:hi]),
-                            np.ascontiguousarray(lam0[:, :, lo:hi]), np.ascontiguousarray(v0[..., lo:hi]),
-                            iterations, inner_iterations, vf)
+        res = compute(np.ascontiguousarray(y[..., lo:hi]), np.ascontiguousarray(P0[:, lo:hi]),
+                      np.ascontiguousarray(lam0[:, :, lo:hi]), np.ascontiguousarray(v0[..., lo:hi]),
+                      iterations, inner_iterations, vf, *((True,) if record_likelihood else ()))
         axes = (1, 2, 3)
     else:
         raise ValueError(f"unknown shard mode {mode!r}")
-    return tuple(_all_gather_concat(np.asarray(a), ax, group, world, device) for a, ax in zip((P, lam, v), axes))
+    out = tuple(_all_gather_concat(np.asarray(a), ax, group, world, device) for a, ax in zip(res[:3], axes))
+    if not record_likelihood:
+        return out
+    ll = np.asarray(res[3], dtype=np.float64)
+    if mode == "mixtures":
+        ll = _all_gather_concat(ll, 0, group, world, device)
+    else:
+        import torch
+
+        t = torch.from_numpy(np.ascontiguousarray(ll)).to(device)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        ll = t.cpu().numpy()
+    return out + (ll,)
 
 
 def _ndev() -> int:

@@ -430,3 +430,26 @@ def test_counters_match_paper_at_benchmark_size():
     y, P0, lam0, v0, _ = mixture(1, 3, 3, 512, 8)
     run = fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=1)
     assert run.counters.inversions == 2048 and run.counters.matmuls == 0
+
+
+def test_sharded_driver_device_path_world1():
+    # the multi-GPU driver's device compute path (gloo world of 1 on this box)
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1805_09498_b200.multigpu import run_fastfca_sharded
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        parts = [mixture(300 + u, 3, 3, 11, 40) for u in range(2)]
+        y, P0, lam0, v0 = (np.stack([p[k] for p in parts]) for k in range(4))
+        for mode in ("mixtures", "bins"):
+            P, lam, v, ll = run_fastfca_sharded(y, P0, lam0, v0, iterations=3, mode=mode, record_likelihood=True)
+            Pr, lr, vr, llr = fastfca.run_fastfca_batch(y, P0, lam0, v0, iterations=3, record_likelihood=True)
+            assert np.array_equal(P, Pr) and np.array_equal(v, vr) and np.allclose(ll, llr, rtol=1e-14)
+    finally:
+        dist.destroy_process_group()

@@ -15,12 +15,17 @@ import torch.multiprocessing as mp
 from paper_1805_09498_b200.multigpu import run_fastfca_sharded, shard_range
 
 
-def _oracle_compute(y, P0, lam0, v0, iterations, inner, v_floor):
+def _oracle_compute(y, P0, lam0, v0, iterations, inner, v_floor, record=False):
     from oracle import fastfca_ref
 
     outs = [fastfca_ref.run_fastfca(y[u], P0[u], lam0[u], v0[u], iterations=iterations,
-                                    inner_iterations=inner, stats=False) for u in range(y.shape[0])]
-    return (np.stack([o.P for o in outs]), np.stack([o.lam for o in outs]), np.stack([o.v for o in outs]))
+                                    inner_iterations=inner, stats=False, record_likelihood=record)
+            for u in range(y.shape[0])]
+    res = (np.stack([o.P for o in outs]), np.stack([o.lam for o in outs]), np.stack([o.v for o in outs]))
+    if record:
+        ll = np.stack([np.array([o.loglik_init] + o.loglik_after_em + o.loglik_after_p) for o in outs])
+        return res + (ll,)
+    return res
 
 
 def _inputs():
@@ -35,8 +40,9 @@ def _worker(rank, world, port, mode, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         y, P0, lam0, v0 = _inputs()
-        P, lam, v = run_fastfca_sharded(y, P0, lam0, v0, iterations=3, mode=mode, compute=_oracle_compute)
-        q.put((rank, P, lam, v))
+        P, lam, v, ll = run_fastfca_sharded(y, P0, lam0, v0, iterations=3, mode=mode, compute=_oracle_compute,
+                                            record_likelihood=True)
+        q.put((rank, P, lam, v, ll))
     finally:
         dist.destroy_process_group()
 
@@ -69,8 +75,8 @@ def test_gloo_world2_matches_unsharded(mode):
         p.join(timeout=60)
         assert p.exitcode == 0
     y, P0, lam0, v0 = _inputs()
-    ref = _oracle_compute(y, P0, lam0, v0, 3, 1, None)
-    for _, P, lam, v in res:
-        for got, want in zip((P, lam, v), ref):
+    ref = _oracle_compute(y, P0, lam0, v0, 3, 1, None, True)
+    for _, P, lam, v, ll in res:
+        for got, want in zip((P, lam, v, ll), ref):
             assert got.shape == want.shape
             assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
