@@ -194,6 +194,17 @@ int ffca_back_transform_phi(int device, void* stream, int mem, int dtype, int U,
 int ffca_params_from_covariances(int device, void* stream, int mem, int dtype, int U, int I, int J, int F,
                                  const void* S_hat, void* P_out, void* lam_out, int* status);
 
+/* STFT analysis (stft.analyze, stft.py:96-112): audio (I, S) real -> (I, N, L/2) complex with
+ * N = (S - L) / shift + 1, sqrt-Hann window, DC and Nyquist packed into bin 0.  dtype selects
+ * float64 -> complex128 or float32 -> complex64.  cuFFT batched R2C. */
+int ffca_stft_analyze(int device, void* stream, int mem, int dtype, int I, long long S, int L, int shift,
+                      const void* audio, void* out);
+
+/* STFT synthesis (stft.synthesize, stft.py:115-134): (I, N, L/2) complex -> (I, (N-1)*shift + L)
+ * real by windowed overlap-add (deterministic gather).  cuFFT batched C2R. */
+int ffca_stft_synthesize(int device, void* stream, int mem, int dtype, int I, int N, int L, int shift,
+                         const void* in, void* audio);
+
 /* Launch plan of the loop kernel for a shape: out6 = {G, C, NL, threads, resident, smem}. */
 int ffca_plan_loop(int device, int dtype, int U, int I, int J, int N, int F, int vf_mode, int* out6);
 

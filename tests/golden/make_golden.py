@@ -108,6 +108,15 @@ def main():
         "step/S01": fastfca.reconstruct_spatial_covariance(params, 1, 2),
     })
 
+    # --- STFT filterbank (the caller of the path)
+    from fcasep.stft import StftConfig, analyze, synthesize
+    rngs = np.random.default_rng(10)
+    audio = rngs.standard_normal((2, 6 * 1024 + 300))
+    cfg = StftConfig()
+    tens = analyze(audio, cfg)
+    out.update({"stft/audio": audio, "stft/obs": tens.data, "stft/resynth": synthesize(tens, cfg),
+                "stft/small_obs": analyze(audio[:, :2048], StftConfig(256, 128)).data})
+
     # --- conventional FCA
     I, J, F, N = 3, 3, 6, 24
     y, P0, lam0, v0, _ = mixture(21, I, J, F, N)

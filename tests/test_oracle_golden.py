@@ -9,7 +9,7 @@ import pytest
 
 from conftest import rel
 from oracle import fastfca_ref as ffr
-from oracle import fca_ref
+from oracle import fca_ref, stft_ref
 
 CASES = ["g33", "g44", "g86", "g22", "g12", "g23"]
 
@@ -94,3 +94,11 @@ def test_oracle_singular_P_raises():
     P = np.zeros((2, 2, 2), complex)
     with pytest.raises(ffr.OracleSingular):
         ffr.run_fastfca(y, P, np.ones((1, 2, 2)), np.ones((1, 3, 2)), iterations=1)
+
+
+def test_stft_oracle_matches_reference(golden):
+    g = {k.split("/", 1)[1]: v for k, v in golden.items() if k.startswith("stft/")}
+    obs = stft_ref.analyze(g["audio"])
+    assert rel(obs, g["obs"]) <= 1e-13
+    assert rel(stft_ref.synthesize(obs), g["resynth"]) <= 1e-13
+    assert rel(stft_ref.analyze(g["audio"][:, :2048], 256, 128), g["small_obs"]) <= 1e-13
