@@ -194,6 +194,17 @@ int ffca_back_transform_phi(int device, void* stream, int mem, int dtype, int U,
 int ffca_params_from_covariances(int device, void* stream, int mem, int dtype, int U, int I, int J, int F,
                                  const void* S_hat, void* P_out, void* lam_out, int* status);
 
+/* Initial covariances (scene.oracle_covariances / scene.diffuse_covariances, scene.py:207-247), one CTA
+ * per (mixture, source, bin) or (mixture, bin), fp64 accumulation:
+ *   mode 0 (oracle):  x = source-image STFTs (U,J,I,N,F); v_hat = max(sum_i |x_i|^2 / I, floor),
+ *                     S_hat = sum_n x x^H / v_hat / N
+ *   mode 1 (diffuse): x = observations (U,I,N,F); S_hat_j = avg + 0.5 max(tr(avg)/I, 1e-300) W_j with
+ *                     W (J,I,I) the seeded trace-normalised PD perturbations; v_hat = max(power / J, floor)
+ * then diagonal loading 1e-9 tr/I (identity when tr <= 0, scene._load_pd, scene.py:200-204).
+ * floor (U,F) float64 from ffca_power_floor.  Outputs S_hat (U,J,F,I,I), v_hat (U,J,N,F). */
+int ffca_init_covariances(int device, void* stream, int mem, int dtype, int mode, int U, int I, int J, int N, int F,
+                          const void* x, const double* floor, const void* W, void* S_out, void* v_out);
+
 /* STFT analysis (stft.analyze, stft.py:96-112): audio (I, S) real -> (I, N, L/2) complex with
  * N = (S - L) / shift + 1, sqrt-Hann window, DC and Nyquist packed into bin 0.  dtype selects
  * float64 -> complex128 or float32 -> complex64.  cuFFT batched R2C. */

@@ -488,22 +488,50 @@ __global__ void __launch_bounds__(128) fca_mstep_kernel(const FcaMstepArgs a) {
   }
 }
 
+// np.abs(y) ** 2 (fca.py:88): hypot then square for complex128; for complex64 the fp64
+// x^2 + y^2 of fp32 components is exact up to one rounding (more accurate than hypot^2).
+__device__ __forceinline__ double abs2_ref(double2 z) {
+  const double m = hypot(z.x, z.y);
+  return m * m;
+}
+__device__ __forceinline__ double abs2_ref(float2 z) {
+  return fma(double(z.x), double(z.x), double(z.y) * double(z.y));
+}
+
+// One CTA per (mixture, tile of 32 bins): lanes own consecutive bins (coalesced rows of the
+// (I, N, F) layout), 8 warps split the frames, fixed-order combine in shared memory.
 template <typename R>
-__global__ void power_floor_kernel(const void* yv, double* out, int U, int I, int N, int F) {
+__global__ void __launch_bounds__(256) power_floor_kernel(const void* yv, double* out, int U, int I, int N, int F) {
   using C2 = typename Cpx<R>::T;
-  const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= (long long)U * F) return;
-  const long long u = b / F;
-  const int f = int(b % F);
+  const int lane = threadIdx.x & 31, ng = threadIdx.x >> 5;
+  const int ftiles = (F + 31) / 32;
+  const long long u = blockIdx.x / ftiles;
+  const int f = int(blockIdx.x % ftiles) * 32 + lane;
   const C2* y = (const C2*)yv;
   double s = 0.0;
-  for (int i = 0; i < I; ++i)
-    for (int n = 0; n < N; ++n) {
-      const C2 z = y[((u * I + i) * N + n) * (long long)F + f];
-      const double m = hypot(double(z.x), double(z.y));
-      s += m * m;
+  if (f < F) {
+    const C2* __restrict__ yp = y + u * I * (long long)N * F + f;
+    const long long rows = (long long)I * N;  // (i, n) rows are contiguous: one flat frame index
+    long long r = ng;
+    for (; r + 24 < rows; r += 32) {  // 4 rows in flight per thread
+      C2 z[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) z[k] = yp[(r + 8 * k) * F];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) s += abs2_ref(z[k]);
     }
-  out[b] = fmax(1e-10 * (s / (double(I) * N)), 1e-300);
+    for (; r < rows; r += 8) {
+      s += abs2_ref(yp[r * F]);
+    }
+  }
+  __shared__ double red[8][32];
+  red[ng][lane] = s;
+  __syncthreads();
+  if (ng != 0 || f >= F) return;
+  double t = red[0][lane];
+#pragma unroll
+  for (int g = 1; g < 8; ++g) t += red[g][lane];
+  out[u * F + f] = fmax(1e-10 * (t / (double(I) * N)), 1e-300);
 }
 
 template <typename R>
@@ -573,9 +601,9 @@ extern "C" int ffca_power_floor(int device, void* stream, int mem, int dtype, in
   FFCA_TRY(st.in(y, size_t(U) * I * N * F * csize(dtype), &dy));
   FFCA_TRY(st.out(out, size_t(nb) * 8, &dout));
   if (dtype == FFCA_C64)
-    power_floor_kernel<float><<<unsigned((nb + 127) / 128), 128, 0, s>>>(dy, (double*)dout, U, I, N, F);
+    power_floor_kernel<float><<<unsigned(U * ((F + 31) / 32)), 256, 0, s>>>(dy, (double*)dout, U, I, N, F);
   else
-    power_floor_kernel<double><<<unsigned((nb + 127) / 128), 128, 0, s>>>(dy, (double*)dout, U, I, N, F);
+    power_floor_kernel<double><<<unsigned(U * ((F + 31) / 32)), 256, 0, s>>>(dy, (double*)dout, U, I, N, F);
   count_launch();
   FFCA_CK(cudaGetLastError());
   FFCA_TRY(st.flush());

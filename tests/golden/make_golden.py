@@ -134,6 +134,24 @@ def main():
         "fca/images": wiener.mmse_images_fca(rf.params, obs).stft,
     })
 
+    # --- initialisers (scene.oracle_covariances / diffuse_covariances), with degenerate bins
+    from fcasep import scene
+    rngi = np.random.default_rng(31)
+    J, I, N, F = 2, 3, 40, 9
+    refs = (rngi.standard_normal((J, I, N, F)) + 1j * rngi.standard_normal((J, I, N, F))) * \
+        rngi.uniform(0.1, 3.0, (J, 1, N, F))
+    refs[:, :, :, 2] = 0.0          # silent bin: floor 1e-300, identity loading
+    refs[1, :, :, 5] = 0.0          # one silent source in a live bin
+    refs[0, :, 7, :] = 0.0          # a silent frame
+    obs_i = ObservationTensor(refs.sum(axis=0))
+    So, vo = scene.oracle_covariances(refs, obs_i)
+    Sd2, vd2 = scene.diffuse_covariances(obs_i, 2, 7)
+    Sd3, vd3 = scene.diffuse_covariances(obs_i, 3, 8)
+    out.update({
+        "scene/refs": refs, "scene/y": obs_i.data, "scene/oracle_S": So, "scene/oracle_v": vo,
+        "scene/diffuse2_S": Sd2, "scene/diffuse2_v": vd2, "scene/diffuse3_S": Sd3, "scene/diffuse3_v": vd3,
+    })
+
     path = os.path.join(HERE, "golden.npz")
     np.savez_compressed(path, **out)
     print(f"wrote {path}: {len(out)} arrays, {os.path.getsize(path) / 1e6:.2f} MB")

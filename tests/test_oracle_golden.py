@@ -9,7 +9,7 @@ import pytest
 
 from conftest import rel
 from oracle import fastfca_ref as ffr
-from oracle import fca_ref, stft_ref
+from oracle import fca_ref, scene_ref, stft_ref
 
 CASES = ["g33", "g44", "g86", "g22", "g12", "g23"]
 
@@ -102,3 +102,14 @@ def test_stft_oracle_matches_reference(golden):
     assert rel(obs, g["obs"]) <= 1e-13
     assert rel(stft_ref.synthesize(obs), g["resynth"]) <= 1e-13
     assert rel(stft_ref.analyze(g["audio"][:, :2048], 256, 128), g["small_obs"]) <= 1e-13
+
+
+def test_scene_initialisers_match_reference(golden):
+    g = {k.split("/", 1)[1]: v for k, v in golden.items() if k.startswith("scene/")}
+    S, v = scene_ref.oracle_covariances(g["refs"], g["y"])
+    assert rel(S, g["oracle_S"]) <= 1e-13 and rel(v, g["oracle_v"]) <= 1e-14
+    # the silent bin falls back to identity loading, exactly as the reference
+    assert np.array_equal(S[:, 2], np.broadcast_to(np.eye(3), S[:, 2].shape))
+    for J, seed in ((2, 7), (3, 8)):
+        S, v = scene_ref.diffuse_covariances(g["y"], J, seed)
+        assert rel(S, g[f"diffuse{J}_S"]) <= 1e-13 and rel(v, g[f"diffuse{J}_v"]) <= 1e-14
