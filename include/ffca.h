@@ -205,6 +205,13 @@ int ffca_params_from_covariances(int device, void* stream, int mem, int dtype, i
 int ffca_init_covariances(int device, void* stream, int mem, int dtype, int mode, int U, int I, int J, int N, int F,
                           const void* x, const double* floor, const void* W, void* S_out, void* v_out);
 
+/* SDR energies for evalkit.compute_sdr (evalkit.py:68-88): ref (J,I,Sr), est (J,I,Se) real
+ * (C128 -> float64, C64 -> float32); out (J,2) float64 = (||ref||^2, ||ref - est||^2) summed over
+ * channels and the first min(Sr, Se) samples.  The dB value and its cap / zero-reference error are
+ * the caller's scalar arithmetic. */
+int ffca_sdr_energies(int device, void* stream, int mem, int dtype, int J, int I, long long Sr, long long Se,
+                      const void* ref, const void* est, double* out);
+
 /* STFT analysis (stft.analyze, stft.py:96-112): audio (I, S) real -> (I, N, L/2) complex with
  * N = (S - L) / shift + 1, sqrt-Hann window, DC and Nyquist packed into bin 0.  dtype selects
  * float64 -> complex128 or float32 -> complex64.  cuFFT batched R2C. */

@@ -15,4 +15,4 @@ All arithmetic is float64 / complex128 (the reference has no 32-bit path,
 ``SPEC.md:146``); the complex64 oracle is this code on exactly-upcast inputs.
 """
 
-from . import fastfca_ref, fca_ref, scene_ref, stft_ref  # noqa: F401
+from . import fastfca_ref, fca_ref, pipeline_ref, scene_ref, stft_ref  # noqa: F401

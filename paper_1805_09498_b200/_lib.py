@@ -67,6 +67,7 @@ SIGNATURES = {
     "ffca_back_transform_phi": [_i, _vp, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp],
     "ffca_params_from_covariances": [_i, _vp, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp],
     "ffca_init_covariances": [_i, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp],
+    "ffca_sdr_energies": [_i, _vp, _i, _i, _i, _i, ctypes.c_longlong, ctypes.c_longlong, _vp, _vp, _vp],
     "ffca_stft_analyze": [_i, _vp, _i, _i, _i, ctypes.c_longlong, _i, _i, _vp, _vp],
     "ffca_stft_synthesize": [_i, _vp, _i, _i, _i, _i, _i, _i, _vp, _vp],
     "ffca_mstep_diag": [_i, _vp, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _d, _vp, _vp, _vp],

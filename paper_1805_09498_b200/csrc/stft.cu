@@ -207,3 +207,98 @@ extern "C" int ffca_stft_synthesize(int device, void* stream, int mem, int dtype
   FFCA_CK(cudaStreamSynchronize(s));
   return FFCA_OK;
 }
+
+// ---------------------------------------------------------------------------
+// SDR energies (evalkit.compute_sdr, evalkit.py:68-88): per source j the fp64
+// sums ||s||^2 and ||s - s_hat||^2 over channels and the first L samples.
+// 64 CTAs per source, then a fixed-order combine (deterministic).
+// ---------------------------------------------------------------------------
+namespace ffca {
+
+constexpr int SDR_CHUNKS = 64;  // CTAs per source; partials combined in a fixed order
+
+// CTA (chunk c, source j) sums samples [c*L/64, (c+1)*L/64) of every channel.
+template <typename R>
+__global__ void __launch_bounds__(256) sdr_energy_kernel(const R* ref, const R* est, double* part, int I, long long Sr,
+                                                         long long Se, long long L) {
+  const int j = blockIdx.y, c = blockIdx.x;
+  const long long lo = L * c / SDR_CHUNKS, hi = L * (c + 1) / SDR_CHUNKS;
+  double er = 0.0, ee = 0.0;
+  for (int i = 0; i < I; ++i) {
+    const R* r = ref + ((long long)j * I + i) * Sr;
+    const R* e = est + ((long long)j * I + i) * Se;
+    for (long long t = lo + threadIdx.x; t < hi; t += blockDim.x) {
+      const double a = double(r[t]), d = a - double(e[t]);
+      er = fma(a, a, er);
+      ee = fma(d, d, ee);
+    }
+  }
+  __shared__ double sr[8], se[8];
+  for (int o = 16; o >= 1; o >>= 1) {
+    er += __shfl_xor_sync(FULL, er, o);
+    ee += __shfl_xor_sync(FULL, ee, o);
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sr[w] = er;
+    se[w] = ee;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0, y = 0.0;
+    for (int k = 0; k < 8; ++k) {
+      x += sr[k];
+      y += se[k];
+    }
+    part[((long long)j * SDR_CHUNKS + c) * 2] = x;
+    part[((long long)j * SDR_CHUNKS + c) * 2 + 1] = y;
+  }
+}
+
+__global__ void sdr_combine_kernel(const double* part, double* out, int J) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= J) return;
+  double x = 0.0, y = 0.0;
+  for (int c = 0; c < SDR_CHUNKS; ++c) {
+    x += part[((long long)j * SDR_CHUNKS + c) * 2];
+    y += part[((long long)j * SDR_CHUNKS + c) * 2 + 1];
+  }
+  out[2 * j] = x;
+  out[2 * j + 1] = y;
+}
+
+}  // namespace ffca
+
+// ref (J, I, Sr), est (J, I, Se) real (dtype C128 -> float64, C64 -> float32);
+// out (J, 2) float64 = (||ref||^2, ||ref - est||^2) over the first min(Sr, Se) samples.
+extern "C" int ffca_sdr_energies(int device, void* stream, int mem, int dtype, int J, int I, long long Sr,
+                                 long long Se, const void* ref, const void* est, double* out) {
+  reset_launches();
+  if ((dtype != FFCA_C128 && dtype != FFCA_C64) || J < 1 || I < 1 || Sr < 0 || Se < 0 || !ref || !est || !out) {
+    set_error("bad arguments to ffca_sdr_energies");
+    return FFCA_E_ARG;
+  }
+  DeviceGuard dg(device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t rs = rsize(dtype);
+  Staging st(mem, s);
+  const void *dr, *de;
+  void* dout;
+  FFCA_TRY(st.in(ref, size_t(J) * I * Sr * rs, &dr));
+  FFCA_TRY(st.in(est, size_t(J) * I * Se * rs, &de));
+  FFCA_TRY(st.out(out, size_t(J) * 2 * 8, &dout));
+  const long long L = Sr < Se ? Sr : Se;
+  void* part;
+  FFCA_TRY(st.scratch(size_t(J) * SDR_CHUNKS * 2 * 8, &part));
+  const dim3 grid(SDR_CHUNKS, J);
+  if (dtype == FFCA_C128)
+    sdr_energy_kernel<double><<<grid, 256, 0, s>>>((const double*)dr, (const double*)de, (double*)part, I, Sr, Se, L);
+  else
+    sdr_energy_kernel<float><<<grid, 256, 0, s>>>((const float*)dr, (const float*)de, (double*)part, I, Sr, Se, L);
+  sdr_combine_kernel<<<(J + 127) / 128, 128, 0, s>>>((const double*)part, (double*)dout, J);
+  count_launch(2);
+  FFCA_CK(cudaGetLastError());
+  FFCA_TRY(st.flush());
+  FFCA_CK(cudaStreamSynchronize(s));
+  return FFCA_OK;
+}

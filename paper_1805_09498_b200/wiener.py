@@ -1,6 +1,6 @@
-"""Source-image recovery (multichannel Wiener filter) -- wiener.py:20-43 on the GPU.
+"""Source-image recovery (multichannel Wiener filter) -- wiener.py:20-53 on the GPU.
 
-Resynthesis / WAV output are out of scope.
+WAV output (wiener.py:56-79) is file I/O and out of scope.
 """
 
 from __future__ import annotations
@@ -10,7 +10,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import fastfca, fca
-from .stft import ObservationTensor
+from .stft import ObservationTensor, StftConfig, synthesize
 
 
 @dataclass
@@ -44,3 +44,14 @@ def mmse_images_fastfca(params: fastfca.FastFcaParams, stats: fastfca.Transforme
     if src is not None and stats._mu is None and src[1] is params:
         return SeparatedImages(stft=fastfca.images_from_state(src[0], params))
     return SeparatedImages(stft=fastfca.back_transform_means(params.P, stats.mu, images_layout=True))
+
+
+def resynthesize_images(images: SeparatedImages, cfg: StftConfig = StftConfig()) -> SeparatedImages:
+    """Time-domain audio for every source by overlap-add synthesis.  wiener.py:46-53.
+
+    All J x I image channels go through one batched device synthesis call.
+    """
+    J, I, N, F = images.stft.shape
+    flat = ObservationTensor(np.ascontiguousarray(images.stft).reshape(J * I, N, F), check_finite=False)
+    audio = synthesize(flat, cfg)
+    return SeparatedImages(stft=images.stft, audio=audio.reshape(J, I, -1))

@@ -152,6 +152,18 @@ def main():
         "scene/diffuse2_S": Sd2, "scene/diffuse2_v": vd2, "scene/diffuse3_S": Sd3, "scene/diffuse3_v": vd3,
     })
 
+    # --- the whole in-memory pipeline (cli.separate_once): synthetic scene -> separated audio
+    from fcasep import cli
+    built = scene.synth_mixture(scene.SceneSpec(n_sources=2, n_channels=2, duration=0.4, seed=9))
+    out.update({"pipe/mixture": built.mixture, "pipe/references": built.references})
+    for algo in ("fastfca", "fca"):
+        for init in ("oracle", "diffuse"):
+            rc = cli.RunConfig(algorithm=algo, iterations=5, init=init, sources=2, seed=4,
+                               frame_length=256, frame_shift=128)
+            images, report, _run = cli.separate_once(rc, built.mixture, built.references)
+            out[f"pipe/{algo}_{init}_audio"] = images.audio
+            out[f"pipe/{algo}_{init}_sdr"] = np.array(report.sdr_per_source)
+
     path = os.path.join(HERE, "golden.npz")
     np.savez_compressed(path, **out)
     print(f"wrote {path}: {len(out)} arrays, {os.path.getsize(path) / 1e6:.2f} MB")

@@ -9,7 +9,7 @@ import pytest
 
 from conftest import rel
 from oracle import fastfca_ref as ffr
-from oracle import fca_ref, scene_ref, stft_ref
+from oracle import fca_ref, pipeline_ref, scene_ref, stft_ref
 
 CASES = ["g33", "g44", "g86", "g22", "g12", "g23"]
 
@@ -113,3 +113,13 @@ def test_scene_initialisers_match_reference(golden):
     for J, seed in ((2, 7), (3, 8)):
         S, v = scene_ref.diffuse_covariances(g["y"], J, seed)
         assert rel(S, g[f"diffuse{J}_S"]) <= 1e-13 and rel(v, g[f"diffuse{J}_v"]) <= 1e-14
+
+
+@pytest.mark.parametrize("algo", ["fastfca", "fca"])
+@pytest.mark.parametrize("init", ["oracle", "diffuse"])
+def test_pipeline_oracle_matches_reference(golden, algo, init):
+    # cli.separate_once on a synthetic scene (scene.synth_mixture, seed 9), 5 iterations
+    audio, sdrs, _ = pipeline_ref.separate_once(golden["pipe/mixture"], golden["pipe/references"], algo, init,
+                                                sources=2, iterations=5, seed=4, L=256, shift=128)
+    assert rel(audio, golden[f"pipe/{algo}_{init}_audio"]) <= 1e-13
+    assert np.allclose(sdrs, golden[f"pipe/{algo}_{init}_sdr"], rtol=0, atol=1e-10)
