@@ -31,6 +31,7 @@ struct LoopPlan {
   bool resident = true;
   size_t smem = 0, slab = 0;
   long long grid = 0;
+  LoopSmem L;  // the carve-up the kernel reads from its parameters
 };
 
 // Slab budget per CTA: two CTAs per SM fit in the 228 KB shared memory.
@@ -62,6 +63,7 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
     p.threads = choose_threads(G, p.NL, I);
     p.resident = res;
     LoopSmem L(I, J, G, p.NL, p.threads / 32, rsz, vf_mode, res, VMAX);
+    p.L = L;
     p.smem = L.total;
     p.slab = L.slab;
     p.grid = ((total_bins + G - 1) / G) * C;
@@ -71,12 +73,13 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
   if (const char* fp = getenv("FFCA_FORCE_PLAN")) {
     int G = 1, C = 1, res = 1, thr = 0;
     const int nf = sscanf(fp, "%d,%d,%d,%d", &G, &C, &res, &thr);
-    if (nf >= 3 && (G == 1 || G == G0) && (G == 1 || res) && C >= 1 && C <= 8 && (C & (C - 1)) == 0 && C <= N &&
+    if (nf >= 3 && (G == 1 || G == G0 || (G == 2 && G0 == 4)) && (G == 1 || res) && C >= 1 && C <= 8 && (C & (C - 1)) == 0 && C <= N &&
         (C == 1 || G == 1)) {
       fill(G, C, res != 0);
       if (nf == 4 && thr >= 64 && thr <= 256 && thr % 32 == 0 && (I <= 4 || thr >= 8 * (I + 1))) {
         p.threads = thr;
         LoopSmem L(I, J, G, p.NL, thr / 32, rsz, vf_mode, res != 0, VMAX);
+        p.L = L;
         p.smem = L.total;
       }
       if (p.smem <= smem_optin) return FFCA_OK;
@@ -93,6 +96,7 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
     fill(1, 1, false);
     p.threads = 256;
     LoopSmem L(I, J, 1, p.NL, 8, rsz, vf_mode, false, VMAX);
+    p.L = L;
     p.smem = L.total;
     if (p.smem <= smem_optin) return FFCA_OK;
   }
@@ -169,6 +173,7 @@ static int launch_problem(int device, const DevProblem& d, cudaStream_t s) {
   a.status = d.status;
   a.scratch = scratch;
   a.slab_bytes = (long long)p.slab;
+  a.L = p.L;
   LoopFn fn = d.dtype == FFCA_C64 ? loop_kernel_f32(d.I, d.J, p.G, p.resident)
                                   : loop_kernel_f64(d.I, d.J, p.G, p.resident);
   if (!fn) {

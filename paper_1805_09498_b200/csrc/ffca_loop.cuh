@@ -27,30 +27,7 @@
 
 namespace ffca {
 
-struct LoopArgs {
-  int U, I, J, N, F;
-  long long total_bins;
-  int G;         // bins per cluster (lane-interleaved), power of two <= 4
-  int C;         // cluster size (CTAs sharing one bin group, split over n)
-  int NL;        // max frames held by one CTA (ceil(N / C))
-  int iters, K;
-  int p_only;    // skip the EM sweep: fixed_point_update_P (fastfca.py:197-237)
-  int vf_mode;   // 0 scalar, 1 per-bin (U,F), 2 full (U,J,N,F), 3 auto (power floor)
-  double vf_scalar;
-  const void* vf;      // real array for modes 1, 2
-  const void* y;       // (U, I, N, F) complex
-  const void* P_in;    // (U, F, I, I) complex
-  const void* lam_in;  // (U, J, F, I) real
-  const void* v_in;    // (U, J, N, F) real
-  void* P_out;
-  void* lam_out;
-  void* v_out;
-  double* vf_out;      // optional (U, F): the floor actually used
-  double* ll;          // optional (total_bins, 1 + 2*iters): per-bin likelihood parts
-  int* status;         // (total_bins)
-  void* scratch;       // non-resident slab storage (slab_bytes per CTA)
-  long long slab_bytes;
-};
+
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 __host__ __device__ constexpr int odd_up(int x) { return (x & 1) ? x : x + 1; }
@@ -81,6 +58,7 @@ __host__ __device__ constexpr int loop_vmax() {
 struct LoopSmem {
   size_t y, v, vf, Pc, Pd, Pinv, lamc, lamd, vfl, ldet, wpart, cpart, tot, bst, M, piv, rhs, total, slab;
   size_t ybytes, vbytes;
+  LoopSmem() = default;
   __host__ __device__ LoopSmem(int I, int J, int G, int NL, int W, int rsz, int vf_mode, bool resident,
                                int VMAX) {
     size_t o = 0;
@@ -121,6 +99,33 @@ struct LoopSmem {
 };
 
 // Sum over the lanes of one bin (lanes sharing lane % G).
+struct LoopArgs {
+  int U, I, J, N, F;
+  long long total_bins;
+  int G;         // bins per cluster (lane-interleaved), power of two <= 4
+  int C;         // cluster size (CTAs sharing one bin group, split over n)
+  int NL;        // max frames held by one CTA (ceil(N / C))
+  int iters, K;
+  int p_only;    // skip the EM sweep: fixed_point_update_P (fastfca.py:197-237)
+  int vf_mode;   // 0 scalar, 1 per-bin (U,F), 2 full (U,J,N,F), 3 auto (power floor)
+  double vf_scalar;
+  const void* vf;      // real array for modes 1, 2
+  const void* y;       // (U, I, N, F) complex
+  const void* P_in;    // (U, F, I, I) complex
+  const void* lam_in;  // (U, J, F, I) real
+  const void* v_in;    // (U, J, N, F) real
+  void* P_out;
+  void* lam_out;
+  void* v_out;
+  double* vf_out;      // optional (U, F): the floor actually used
+  double* ll;          // optional (total_bins, 1 + 2*iters): per-bin likelihood parts
+  int* status;         // (total_bins)
+  void* scratch;       // non-resident slab storage (slab_bytes per CTA)
+  long long slab_bytes;
+  LoopSmem L;          // shared-memory carve-up, computed once on the host (kernel reads it from
+                       // the constant bank instead of re-deriving offsets in registers)
+};
+
 template <int G, typename T>
 __device__ __forceinline__ T bin_warp_sum(T x) {
 #pragma unroll
@@ -573,8 +578,8 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
   extern __shared__ __align__(16) unsigned char smem[];
   const int W = blockDim.x >> 5;
   const bool resident = RES || a.scratch == nullptr;
-  const LoopSmem L(I, J, G, a.NL, W, sizeof(R), a.vf_mode, resident, VMAX);
-  // the host sized the launch with the same carve-up; trap rather than run past it
+  const LoopSmem& L = a.L;
+  // the host sized the launch with this carve-up; trap rather than run past it
   if (L.total > dynamic_smem_bytes()) __trap();
 
   int crank = 0;

@@ -12,6 +12,8 @@ template <int I, int J>
 static LoopFn hot(int G, bool res) {
   if constexpr (I <= 4) {
     if (G == 4 && res) return ffca_loop_kernel<float, I, J, 4, true>;
+    if constexpr (I == 3 && J == 3)
+      if (G == 2 && res) return ffca_loop_kernel<float, I, J, 2, true>;
   }
   if (G == 1) return res ? (LoopFn)ffca_loop_kernel<float, I, J, 1, true> : (LoopFn)ffca_loop_kernel<float, I, J, 1, false>;
   return nullptr;
