@@ -164,6 +164,10 @@ def main():
             out[f"pipe/{algo}_{init}_audio"] = images.audio
             out[f"pipe/{algo}_{init}_sdr"] = np.array(report.sdr_per_source)
 
+    # --- synthetic scene generator (scene.synth_mixture), used by the acceptance tests
+    sc = scene.synth_mixture(scene.SceneSpec(n_sources=2, n_channels=3, duration=0.25, seed=5))
+    out.update({"scenegen/mixture": sc.mixture, "scenegen/references": sc.references})
+
     path = os.path.join(HERE, "golden.npz")
     np.savez_compressed(path, **out)
     print(f"wrote {path}: {len(out)} arrays, {os.path.getsize(path) / 1e6:.2f} MB")

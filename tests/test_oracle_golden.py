@@ -123,3 +123,9 @@ def test_pipeline_oracle_matches_reference(golden, algo, init):
                                                 sources=2, iterations=5, seed=4, L=256, shift=128)
     assert rel(audio, golden[f"pipe/{algo}_{init}_audio"]) <= 1e-13
     assert np.allclose(sdrs, golden[f"pipe/{algo}_{init}_sdr"], rtol=0, atol=1e-10)
+
+
+def test_scene_generator_matches_reference(golden):
+    mix, refs = scene_ref.synth_mixture(n_sources=2, n_channels=3, duration=0.25, seed=5)
+    assert rel(mix, golden["scenegen/mixture"]) <= 1e-13
+    assert rel(refs, golden["scenegen/references"]) <= 1e-13
