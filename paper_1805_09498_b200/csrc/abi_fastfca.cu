@@ -73,7 +73,7 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
   if (const char* fp = getenv("FFCA_FORCE_PLAN")) {
     int G = 1, C = 1, res = 1, thr = 0;
     const int nf = sscanf(fp, "%d,%d,%d,%d", &G, &C, &res, &thr);
-    if (nf >= 3 && (G == 1 || G == G0 || (G == 2 && G0 == 4)) && (G == 1 || res) && C >= 1 && C <= 8 && (C & (C - 1)) == 0 && C <= N &&
+    if (nf >= 3 && (G == 1 || G == G0 || (G == 2 && G0 == 4)) && (G == 1 || res) && C >= 1 && C <= 16 && (C & (C - 1)) == 0 && C <= N &&
         (C == 1 || G == 1)) {
       fill(G, C, res != 0);
       if (nf == 4 && thr >= 64 && thr <= 256 && thr % 32 == 0 && (I <= 4 || thr >= 8 * (I + 1))) {
@@ -115,6 +115,7 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
 
 static int launch_loop(LoopFn fn, const LoopPlan& p, const LoopArgs& a, cudaStream_t s) {
   FFCA_CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p.smem)));
+  if (p.C > 8) FFCA_CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(p.grid), 1, 1);
   cfg.blockDim = dim3(unsigned(p.threads), 1, 1);
