@@ -225,8 +225,9 @@ struct PointWork {
   const R* lamc;
   int g, J, JS, rec0, rstep, npts;
   R wfl, invI;
+  static constexpr int IP2 = (I + 1) / 2;  // lambda stored as (i, i+1) pairs for FFMA2
   C2 Pr[PREG ? I : 1][PREG ? I : 1];
-  R Lr[PREG ? JM : 1][PREG ? I : 1];
+  C2 Lp[PREG ? JM : 1][PREG ? IP2 : 1];
 
   __device__ __forceinline__ void load_PL() {
     if constexpr (PREG) {
@@ -237,7 +238,11 @@ struct PointWork {
 #pragma unroll
       for (int j = 0; j < JM; ++j)
 #pragma unroll
-        for (int i = 0; i < I; ++i) Lr[j][i] = (j < J) ? lamc[(g * J + j) * I + i] : R(0);
+        for (int ip = 0; ip < IP2; ++ip) {
+          const R l0 = (j < J) ? lamc[(g * J + j) * I + 2 * ip] : R(0);
+          const R l1 = (j < J && 2 * ip + 1 < I) ? lamc[(g * J + j) * I + 2 * ip + 1] : R(0);
+          Lp[j][ip] = mk<C2, R>(l0, l1);
+        }
     }
   }
   __device__ __forceinline__ C2 P(int x, int y2) const {
@@ -245,7 +250,7 @@ struct PointWork {
     else return Pc[(g * I + x) * I + y2];
   }
   __device__ __forceinline__ R Lam(int j, int i) const {
-    if constexpr (PREG) return Lr[j][i];
+    if constexpr (PREG) return (i & 1) ? Lp[j][i >> 1].y : Lp[j][i >> 1].x;
     else return lamc[(g * J + j) * I + i];
   }
   // y_t = P^H y ; q = |y_t|^2   (fastfca.py:442-446)
@@ -260,13 +265,26 @@ struct PointWork {
   }
   // w_i = max(sum_j v_j lambda_ji, floor)   (fastfca.py:324)
   __device__ __forceinline__ void weights(const R (&vj)[JM], R (&w)[I]) const {
+    if constexpr (PREG) {  // (w_i, w_i+1) pairs: one FFMA2 per source and pair
+      C2 s2[IP2];
 #pragma unroll
-    for (int i = 0; i < I; ++i) {
-      R s = R(0);
+      for (int ip = 0; ip < IP2; ++ip) s2[ip] = mk<C2, R>(R(0), R(0));
 #pragma unroll
       for (int j = 0; j < JM; ++j)
-        if (j < J) s = fma(vj[j], Lam(j, i), s);
-      w[i] = fmax(s, wfl);
+        if (j < J)
+#pragma unroll
+          for (int ip = 0; ip < IP2; ++ip) s2[ip] = fma2(bc2<R>(vj[j]), Lp[j][ip], s2[ip]);
+#pragma unroll
+      for (int i = 0; i < I; ++i) w[i] = fmax((i & 1) ? s2[i >> 1].y : s2[i >> 1].x, wfl);
+    } else {
+#pragma unroll
+      for (int i = 0; i < I; ++i) {
+        R s = R(0);
+#pragma unroll
+        for (int j = 0; j < JM; ++j)
+          if (j < J) s = fma(vj[j], Lam(j, i), s);
+        w[i] = fmax(s, wfl);
+      }
     }
   }
   __device__ __forceinline__ void load_point(const C2* yp, const R* vp, C2 (&yv)[I], R (&vj)[JM]) const {
@@ -319,31 +337,28 @@ struct PointWork {
       }
       R w[I];
       weights(vj, w);
-      // Qi = (1/w_i, q_i/w_i^2)
-      P2 Q[I];
+      // d_i = q_i / w_i^2 - 1 / w_i, so that r2_j - r1_j = sum_i lambda_ji d_i
+      R iw[I], d[I];
 #pragma unroll
       for (int i = 0; i < I; ++i) {
-        const R iw = rcp_pt(w[i]);
-        Q[i] = mk<C2, R>(iw, (q[i] * iw) * iw);
+        iw[i] = rcp_pt(w[i]);
+        d[i] = fma(q[i], iw[i], R(-1)) * iw[i];
       }
       if constexpr (REC) {
 #pragma unroll
-        for (int i = 0; i < I; ++i) lacc += flog(w[i]) + q[i] * Q[i].x;
+        for (int i = 0; i < I; ++i) lacc += flog(w[i]) + q[i] * iw[i];
       }
-      R d[I];
-#pragma unroll
-      for (int i = 0; i < I; ++i) d[i] = Q[i].y - Q[i].x;
 #pragma unroll
       for (int j = 0; j < JM; ++j) {
         if (j < J) {
-          P2 rr = mk<C2, R>(R(0), R(0));  // (r1_j, r2_j)
+          R sd = R(0);  // r2_j - r1_j
 #pragma unroll
-          for (int i = 0; i < I; ++i) rr = fma2(Q[i], bc2<R>(Lam(j, i)), rr);
+          for (int i = 0; i < I; ++i) sd = fma(Lam(j, i), d[i], sd);
           const R v = vj[j];
-          const R step = (((rr.x - rr.y) * v) * v) * invI;
           R fl = vfl_b;
           if constexpr (VF2) fl = fp[j];
-          const R vn = fmax(v - step, fl);
+          // v' = v - v^2 (r1 - r2) / I   (fastfca.py:336-337)
+          const R vn = fmax(fma(sd, (v * v) * invI, v), fl);
           const R ratio = v * rcp_pt(vn);
           s0[j] += ratio;
           const R rv = ratio * v;
