@@ -29,6 +29,7 @@ static int fca_jm(int I, int J) { return ((I == 3 && J == 3) || (I == 2 && J == 
 struct FcaPlan {
   int C = 1, NL = 0, threads = 64;
   size_t smem = 0;
+  FcaSmem L;
 };
 
 static int plan_fca(int dtype, int I, int J, int N, int vf_mode, FcaPlan& p, size_t optin) {
@@ -46,6 +47,7 @@ static int plan_fca(int dtype, int I, int J, int N, int vf_mode, FcaPlan& p, siz
       if (v >= 64 && v <= 256 && v % 32 == 0) p.threads = v;
     }
     FcaSmem L(I, J, p.NL, p.threads / 32, rsz, vf_mode, VMAX);
+    p.L = L;
     p.smem = L.total;
     if (L.slab <= 100 * 1024 && p.smem <= optin) return FFCA_OK;
   }
@@ -75,7 +77,9 @@ static int fca_launch(int device, int dtype, const FcaArgs& a, cudaStream_t s, c
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  FFCA_CK(cudaLaunchKernelEx(&cfg, fn, a));
+  FcaArgs b = a;
+  b.L = p.L;
+  FFCA_CK(cudaLaunchKernelEx(&cfg, fn, b));
   count_launch();
   return FFCA_OK;
 }

@@ -21,29 +21,13 @@
 
 namespace ffca {
 
-struct FcaArgs {
-  int U, I, J, N, F;
-  long long total_bins;
-  int C, NL;
-  int iters;
-  int vf_mode;  // 0 scalar, 1 per-bin, 2 full, 3 auto
-  double vf_scalar;
-  const void* vf;
-  const void* y;   // (U,I,N,F)
-  const void* S0;  // (U,J,F,I,I)
-  const void* v0;  // (U,J,N,F)
-  void* S_out;
-  void* v_out;
-  void* S_prev;    // optional: S of the last E-step
-  void* v_prev;    // optional: v of the last E-step
-  double* ll;      // optional (total_bins, 1 + iters)
-  int* status;
-};
+
 
 __host__ __device__ constexpr int herm_reals(int I) { return I * I; }
 
 struct FcaSmem {
   size_t y, v0, v1, vf, S, Sd, Si, wpart, cpart, tot, vfl, total, slab;
+  FcaSmem() = default;
   __host__ __device__ FcaSmem(int I, int J, int NL, int W, int rsz, int vf_mode, int VMAX) {
     size_t o = 0;
     const size_t csz = 2 * size_t(rsz);
@@ -61,6 +45,26 @@ struct FcaSmem {
     vfl = o;   o += 16;
     total = o;
   }
+};
+
+struct FcaArgs {
+  int U, I, J, N, F;
+  long long total_bins;
+  int C, NL;
+  int iters;
+  int vf_mode;  // 0 scalar, 1 per-bin, 2 full, 3 auto
+  double vf_scalar;
+  const void* vf;
+  const void* y;   // (U,I,N,F)
+  const void* S0;  // (U,J,F,I,I)
+  const void* v0;  // (U,J,N,F)
+  void* S_out;
+  void* v_out;
+  void* S_prev;    // optional: S of the last E-step
+  void* v_prev;    // optional: v of the last E-step
+  double* ll;      // optional (total_bins, 1 + iters)
+  int* status;
+  FcaSmem L;  // shared-memory carve-up from the host (read from the kernel parameters)
 };
 
 // Packed-lower index helpers: row a starts at a*a; diag first, then (a,b<a) pairs.
@@ -377,7 +381,7 @@ __global__ void __launch_bounds__(256) fca_loop_kernel(const FcaArgs a) {
   const int tid = threadIdx.x;
   extern __shared__ __align__(16) unsigned char smem[];
   const int W = blockDim.x >> 5;
-  const FcaSmem L(I, J, a.NL, W, sizeof(R), a.vf_mode, VMAX);
+  const FcaSmem& L = a.L;
   if (L.total > dynamic_smem_bytes()) __trap();
   int crank = 0;
   if (C > 1) crank = int(cg::this_cluster().block_rank());
