@@ -126,6 +126,8 @@ __device__ __forceinline__ void cp_async(void* smem_dst, const void* gsrc, bool 
     asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(d), "l"(gsrc), "n"(BYTES), "r"(n));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+// L1 prefetch of the line holding a global address (no register result)
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
 // Sum over lanes that share (lane mod G); G is a power of two dividing 32.
 template <typename T>

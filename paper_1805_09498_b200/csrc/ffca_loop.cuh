@@ -224,8 +224,10 @@ struct PointWork {
   const C2* Pc;
   const R* lamc;
   int g, J, JS, rec0, rstep, npts;
+  bool gslab;  // slab in global scratch: prefetch upcoming frames into L1
   R wfl, invI;
   static constexpr int IP2 = (I + 1) / 2;  // lambda stored as (i, i+1) pairs for FFMA2
+  static constexpr int PFD = 2;            // prefetch distance (frames of this thread) on a global slab
   C2 Pr[PREG ? I : 1][PREG ? I : 1];
   C2 Lp[PREG ? JM : 1][PREG ? IP2 : 1];
 
@@ -319,6 +321,10 @@ struct PointWork {
     }
 #pragma unroll 1
     for (int k = 0; k < npts; ++k, yp += rstep * RS, vp += rstep * JS, fp += rstep * JS) {
+      if (gslab && k + PFD < npts) {  // the global slab is L2-latency-bound: fetch PFD frames ahead
+        prefetch_l1(yp + PFD * rstep * RS);
+        prefetch_l1(vp + PFD * rstep * JS);
+      }
       C2 yv[I];
       R vj[JM];
       load_point(yp, vp, yv, vj);
@@ -504,6 +510,11 @@ struct PointWork {
       const int nn = valid ? n : 0;
       const C2* yp = ys + (nn * G + g) * RS;
       const R* vp = vs + (nn * G + g) * JS;
+      if (gslab && n + PFD * stride < NLr && p < 2) {  // two lanes per point: its y and v records
+        const int np = n + PFD * stride;
+        if (p == 0) prefetch_l1(ys + (np * G + g) * RS);
+        else prefetch_l1(vs + (np * G + g) * JS);
+      }
       R iw_own = R(0);
       if (valid && p < I) {
         R s = R(0);
@@ -736,6 +747,7 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
 
   PointWork<R, I, JM, G> pw;
   pw.ys = ys; pw.vs = vs; pw.vfs = vfs; pw.Pc = Pc; pw.lamc = lamc;
+  pw.gslab = !resident;
   pw.g = g; pw.J = J; pw.JS = JS; pw.rec0 = rec0; pw.rstep = rstep; pw.npts = npts;
   pw.wfl = wfl; pw.invI = invI;
 
