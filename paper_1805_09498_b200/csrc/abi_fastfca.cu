@@ -406,7 +406,11 @@ static int loop_entry(int device, void* stream, int mem, int dtype, int U, int I
   const size_t threshold = minb ? size_t(atoll(minb)) : (size_t(64) << 20);
   if (mem == FFCA_MEM_HOST && in_bytes >= threshold && !(nopipe && nopipe[0] == '1')) {
     const bool by_mix = U >= 2;
-    const int nchunk = by_mix ? std::min(U, 8) : std::min(F, 8);
+    // chunks of ~128 MB of input (>= 2, <= 32): short enough that the pipeline's fill and
+    // drain (first H2D, last kernel + D2H) are a small part of the PCIe-bound whole
+    const char* nch_env = getenv("FFCA_PIPELINE_CHUNKS");
+    int want = nch_env ? atoi(nch_env) : int(std::min<size_t>(32, std::max<size_t>(2, in_bytes >> 27)));
+    const int nchunk = by_mix ? std::min(U, want) : std::min(F, want);
     if (nchunk >= 2) {
       return pipelined_host_run(device, s, d, record_likelihood != 0, nchunk, by_mix, y, P0, lam0, v0, vf, P_out, lam_out, v_out,
                                 record_likelihood ? ll_out : nullptr, vf_out, status);
