@@ -154,6 +154,192 @@ __global__ void __launch_bounds__(256) point_kernel(const PointArgs a) {
   }
 }
 
+// Statistics refresh / Wiener images for I <= 4, bin-tiled: a CTA owns 32 consecutive bins of
+// one mixture (lane = bin, so every (i, n) row access is one coalesced 32-bin segment) and its 8
+// warps stride over the frames.  The per-bin constants P, lambda (and Q = P^-H for the images)
+// are loaded into registers once per thread instead of once per point, Q in the compute type.
+// Per point: y_t = P^H y, w = sum_j v_j lambda_j, then per source g = v lambda / w,
+// mu_t = g y_t, phi_t = max(v lambda (1 - g), 0)  (fastfca.py:373-387), or the image
+// x_j = Q mu_t written straight into (U, J, I, N, F)  (wiener.py:38-43).
+constexpr int TILE_F = 32, TILE_WARPS = 8;
+// frames in flight per warp: as many ring stages as fit ~46 KB of static shared memory (<= 4)
+template <typename R, int I>
+constexpr int tile_depth() {
+  constexpr int d = 46 * 1024 / (TILE_WARPS * TILE_F * (2 * I + 4) * int(sizeof(R)));
+  return d > 4 ? 4 : (d < 1 ? 1 : d);
+}
+
+template <typename R, int I, int MODE>
+__global__ void __launch_bounds__(TILE_F* TILE_WARPS, 2) point_tile_kernel(const PointArgs a) {
+  using C2 = typename Cpx<R>::T;
+  constexpr int JMAX = 4;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int F = a.F, N = a.N, J = a.J;
+  const int ftiles = (F + TILE_F - 1) / TILE_F;
+  const long long u = blockIdx.x / ftiles;
+  const int f0 = int(blockIdx.x % ftiles) * TILE_F;
+  const bool live = f0 + lane < F;  // dead lanes of a partial tile compute on a clamped bin, store nothing
+  const int f = live ? f0 + lane : F - 1;
+  const long long bin = u * F + f;
+  const R wfl = Floors<R>::weight;
+  C2 Pm[I][I];
+  const C2* Pg = (const C2*)a.P + bin * I * I;
+#pragma unroll
+  for (int x = 0; x < I; ++x)
+#pragma unroll
+    for (int b = 0; b < I; ++b) Pm[x][b] = Pg[x * I + b];
+  R lam[JMAX][I];
+#pragma unroll
+  for (int j = 0; j < JMAX; ++j)
+#pragma unroll
+    for (int i = 0; i < I; ++i) lam[j][i] = j < J ? ((const R*)a.lam)[((u * J + j) * F + f) * I + i] : R(0);
+  C2 Qm[MODE == PM_IMAGES ? I : 1][MODE == PM_IMAGES ? I : 1];
+  if constexpr (MODE == PM_IMAGES) {
+    const double2* Qg = (const double2*)a.Q + bin * I * I;
+#pragma unroll
+    for (int x = 0; x < I; ++x)
+#pragma unroll
+      for (int b = 0; b < I; ++b) {
+        const double2 q = Qg[x * I + b];
+        Qm[x][b] = mk<C2, R>(R(q.x), R(q.y));
+      }
+  }
+  const long long rowN = (long long)N * F;  // stride between channels / sources
+  const C2* __restrict__ yb = (const C2*)a.y + u * I * rowN;
+  const R* __restrict__ vb = (const R*)a.v + u * J * rowN;
+  constexpr int TILE_D = tile_depth<R, I>();
+  const int nlive = (F - f0) < TILE_F ? (F - f0) : TILE_F;  // bins of this tile
+  // the kernel is load-latency-bound: each warp keeps TILE_D frames of y and v in flight with
+  // cp.async into a per-warp shared-memory ring (each lane reads back only what it copied)
+  // stats: a warp's mu_t (phi_t) for one (source, frame) is one contiguous run of 32*I complex
+  // (reals) in the (..., F, I) layout; it is staged in the ring slot just consumed (y part for
+  // mu, v part for phi: I <= JMAX) and written back as 16-byte vectors, so every store
+  // instruction covers whole sectors.  The slot is refilled only by the next iteration's issue.
+  __shared__ __align__(16) C2 ry[TILE_WARPS][TILE_D][I][TILE_F];
+  __shared__ __align__(16) R rv[TILE_WARPS][TILE_D][JMAX][TILE_F];
+  const int nfr = N > wp ? (N - wp + TILE_WARPS - 1) / TILE_WARPS : 0;  // frames of this warp
+  auto issue = [&](int k) {
+    const int n = wp + k * TILE_WARPS;
+    const bool ok = k < nfr;
+    const long long o = ok ? (long long)n * F + f : 0;
+    const int sl = k % TILE_D;
+#pragma unroll
+    for (int i = 0; i < I; ++i) cp_async<sizeof(C2)>(&ry[wp][sl][i][lane], yb + i * rowN + o, ok);
+#pragma unroll
+    for (int j = 0; j < JMAX; ++j)
+      if (j < J) cp_async<sizeof(R)>(&rv[wp][sl][j][lane], vb + j * rowN + o, ok);
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int k = 0; k < TILE_D - 1; ++k) issue(k);
+#pragma unroll 1
+  for (int k = 0; k < nfr; ++k) {
+    issue(k + TILE_D - 1);
+    cp_async_wait<TILE_D - 1>();
+    const int n = wp + k * TILE_WARPS;
+    const int sl = k % TILE_D;
+    const long long off = (long long)n * F + f;
+    C2 yv[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) yv[i] = ry[wp][sl][i][lane];
+    R vj[JMAX];
+#pragma unroll
+    for (int j = 0; j < JMAX; ++j) vj[j] = j < J ? rv[wp][sl][j][lane] : R(0);
+    C2 yt[I];  // P^H y as pair arithmetic (FFMA2 in fp32)
+#pragma unroll
+    for (int b = 0; b < I; ++b) {
+      C2 acc = mk<C2, R>(R(0), R(0));
+#pragma unroll
+      for (int x = 0; x < I; ++x) {
+        acc = fma2(yv[x], bc2<R>(Pm[x][b].x), acc);                          // p.x (y.x, y.y)
+        acc = fma2(mk<C2, R>(yv[x].y, -yv[x].x), bc2<R>(Pm[x][b].y), acc);  // p.y (y.y, -y.x)
+      }
+      yt[b] = acc;
+    }
+    R iw[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      R w = R(0);
+#pragma unroll
+      for (int j = 0; j < JMAX; ++j)
+        if (j < J) w = fma(vj[j], lam[j][i], w);
+      iw[i] = rcp(fmax(w, wfl));
+    }
+#pragma unroll
+    for (int j = 0; j < JMAX; ++j) {
+      if (j >= J) continue;
+      C2 mu[I];
+      R ph[I];
+#pragma unroll
+      for (int i = 0; i < I; ++i) {
+        const R aa = vj[j] * lam[j][i];
+        const R g = aa * iw[i];
+        mu[i] = fma2(yt[i], bc2<R>(g), mk<C2, R>(R(0), R(0)));
+        ph[i] = fmax(aa * (R(1) - g), R(0));
+      }
+      if constexpr (MODE == PM_STATS) {
+        const long long base = ((u * J + j) * rowN + (long long)n * F + f0) * I;  // first element of the run
+#pragma unroll
+        C2* stage_mu = &ry[wp][sl][0][0];
+        R* stage_phi = &rv[wp][sl][0][0];
+        __syncwarp();  // every lane has read this slot's y / v (and the previous source's run)
+        for (int i = 0; i < I; ++i) {
+          stage_mu[lane * I + i] = mu[i];
+          stage_phi[lane * I + i] = ph[i];
+        }
+        __syncwarp();
+        const int ne = nlive * I;  // complex (real) elements of this run
+        if (a.out0) {
+          C2* o = (C2*)a.out0 + base;
+          constexpr int PER = 16 / sizeof(C2);  // complex per 16-byte vector (2 for c64, 1 for c128)
+          const bool vec = ((reinterpret_cast<uintptr_t>(o) & 15) == 0) && (ne % PER == 0);
+          if (vec) {
+            for (int e = lane; e < ne / PER; e += 32)
+              reinterpret_cast<float4*>(o)[e] = reinterpret_cast<const float4*>(stage_mu)[e];
+          } else {
+            for (int e = lane; e < ne; e += 32) o[e] = stage_mu[e];
+          }
+        }
+        if (a.out1) {
+          R* o = (R*)a.out1 + base;
+          constexpr int PER = 16 / sizeof(R);
+          const bool vec = ((reinterpret_cast<uintptr_t>(o) & 15) == 0) && (ne % PER == 0);
+          if (vec) {
+            for (int e = lane; e < ne / PER; e += 32)
+              reinterpret_cast<float4*>(o)[e] = reinterpret_cast<const float4*>(stage_phi)[e];
+          } else {
+            for (int e = lane; e < ne; e += 32) o[e] = stage_phi[e];
+          }
+        }
+        __syncwarp();
+      } else {
+        C2* __restrict__ out = (C2*)a.out0 + (u * J + j) * I * rowN + off;
+#pragma unroll
+        for (int x = 0; x < I; ++x) {
+          C2 acc = mk<C2, R>(R(0), R(0));
+#pragma unroll
+          for (int b = 0; b < I; ++b) {  // acc += Q[x][b] mu[b] = q.x (mu.x, mu.y) + q.y (-mu.y, mu.x)
+            acc = fma2(mu[b], bc2<R>(Qm[x][b].x), acc);
+            acc = fma2(mk<C2, R>(-mu[b].y, mu[b].x), bc2<R>(Qm[x][b].y), acc);
+          }
+          if (live) out[x * rowN] = acc;
+        }
+      }
+    }
+  }
+}
+
+template <typename R, int MODE>
+static void* tile_fn(int I) {
+  switch (I) {
+    case 1: return (void*)point_tile_kernel<R, 1, MODE>;
+    case 2: return (void*)point_tile_kernel<R, 2, MODE>;
+    case 3: return (void*)point_tile_kernel<R, 3, MODE>;
+    case 4: return (void*)point_tile_kernel<R, 4, MODE>;
+  }
+  return nullptr;
+}
+
 // Q = P^-H per bin (one thread per bin, fp64, LU from common.cuh in a
 // per-thread local workspace).  Flags exactly singular P.
 template <typename R, int I>
@@ -215,6 +401,18 @@ static void* inv_fn(int I) {
 int launch_points(int dtype, const PointArgs& a, cudaStream_t s) {
   const long long npts = (long long)a.U * a.N * a.F;
   if (npts == 0) return FFCA_OK;
+  if ((a.mode == PM_STATS || a.mode == PM_IMAGES) && a.I <= 4 && a.J <= 4) {
+    void* tf = nullptr;
+    if (a.mode == PM_STATS)
+      tf = dtype == FFCA_C64 ? tile_fn<float, PM_STATS>(a.I) : tile_fn<double, PM_STATS>(a.I);
+    else
+      tf = dtype == FFCA_C64 ? tile_fn<float, PM_IMAGES>(a.I) : tile_fn<double, PM_IMAGES>(a.I);
+    const long long blocks = (long long)a.U * ((a.F + TILE_F - 1) / TILE_F);
+    void* args[] = {(void*)&a};
+    FFCA_CK(cudaLaunchKernel(tf, dim3(unsigned(blocks)), dim3(TILE_F * TILE_WARPS), args, 0, s));
+    count_launch();
+    return FFCA_OK;
+  }
   void* fn = dtype == FFCA_C64 ? point_fn<float>(a.I) : point_fn<double>(a.I);
   if (!fn) {
     set_error("unsupported order I=%d", a.I);
