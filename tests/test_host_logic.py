@@ -78,3 +78,46 @@ def test_channel_mismatch_raises_before_any_device_call():
     params = fastfca.FastFcaParams(np.broadcast_to(np.eye(3), (4, 3, 3)), np.ones((1, 4, 3)), np.ones((1, 3, 4)))
     with pytest.raises(errors.DimensionMismatch):
         fastfca.run_fastfca(obs, params, iterations=1)
+
+
+# The reference package's public names (fcasep/__init__.py:11-58) and the module-level functions of
+# the modules on the path; the drop-in must expose every one of them.
+REF_EXPORTS = ["ChannelCountMismatch", "ChannelLengthMismatch", "DimensionMismatch", "EvalReport", "FcaParams",
+               "FcasepError", "FastFcaParams", "LengthMismatch", "NotPositiveDefinite", "ObservationTensor",
+               "OpCounters", "PosteriorStats", "SampleRateMismatch", "SingularP", "SingularWeightedCovariance",
+               "StftConfig", "TooShort", "TransformedStats", "ZeroReference", "analyze", "compute_sdr",
+               "expected_counts", "measure_rtf", "run_fca", "run_fastfca", "synthesize"]
+REF_MODULE_API = {
+    "fastfca": ["FastFcaParams", "TransformedStats", "FastFcaRun", "transform_observations",
+                "reconstruct_spatial_covariances", "reconstruct_spatial_covariance", "mixture_weights", "e_step_diag",
+                "m_step_diag", "fixed_point_update_P", "log_likelihood", "back_transform_means",
+                "back_transform_stats", "params_from_covariances", "run_fastfca"],
+    "fca": ["FcaParams", "PosteriorStats", "FcaRun", "power_floor", "mix_covariance", "log_likelihood", "e_step",
+            "m_step", "run_fca"],
+    "wiener": ["SeparatedImages", "mmse_images_fca", "mmse_images_fastfca", "resynthesize_images"],
+    "stft": ["StftConfig", "ObservationTensor", "analyze", "synthesize", "interior_slice"],
+    "scene": ["INIT_LOADING", "oracle_covariances", "diffuse_covariances", "init_oracle", "init_diffuse",
+              "reference_tensors"],
+    "evalkit": ["OpCounters", "expected_counts", "compute_sdr", "rtf_value", "measure_rtf", "EvalReport"],
+}
+
+
+def test_drop_in_exports_every_reference_name():
+    import importlib
+
+    import paper_1805_09498_b200 as pkg
+
+    assert [n for n in REF_EXPORTS if not hasattr(pkg, n)] == []
+    for mod, names in REF_MODULE_API.items():
+        m = importlib.import_module(f"paper_1805_09498_b200.{mod}")
+        assert [n for n in names if not hasattr(m, n)] == [], mod
+
+
+def test_eval_report_rows_and_summary():
+    from paper_1805_09498_b200.evalkit import EvalReport, OpCounters
+
+    r = EvalReport("fastfca", 3, 3, 249, 512, 20, 1, 1e-4, [5.0, 7.0], OpCounters(40960, 0), trial=1, seed=3,
+                   extras={"rtf_ratio_measured": "1.3"})
+    row = r.row()
+    assert row["sdr_mean"] == "6.000000" and row["sdr_2"] == "7.000000" and row["inversions"] == 40960
+    assert row["rtf_ratio_measured"] == "1.3" and "fastfca: I=3 J=3" in r.summary()
