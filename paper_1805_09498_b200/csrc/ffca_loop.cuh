@@ -877,6 +877,7 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
       // publishes the factors; s = 1 + i factors B_i = L D L^H in registers.
       // After one barrier every s >= 1 thread forms [P^-H]_i = conj(row i of
       // P^-1) from the shared LU and solves B_i x = [P^-H]_i itself.
+      static_assert(G * (I + 1) <= 32, "the per-bin solver threads must be lanes of one warp");
       const int s = tid % (I + 1);
       const int gg = tid / (I + 1);
       const long long b = group * G + gg;
@@ -928,7 +929,10 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
             pv[x] = lu.piv[x];
           }
         }
-        __syncthreads();
+        // all G*(I+1) <= 20 solver threads are lanes of warp 0: a warp barrier orders the
+        // LU publication (and, below, the column updates) -- the other warps go straight on
+        // to the block barrier after the loop
+        __syncwarp();
         if (bact && s > 0) {
           const int i = s - 1;
           SmallLU<I> lu;
@@ -950,8 +954,9 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
             Pc[(gg * I + x) * I + i] = mk<C2, R>(R(z[x].x), R(z[x].y));
           }
         }
-        __syncthreads();
+        __syncwarp();
       }
+      __syncthreads();
     } else {
       // I > 4: one group of 8 lanes per system (G == 1).  Group 0 inverts P,
       // groups 1..I invert B_i, all concurrently (Gauss-Jordan, row per lane);

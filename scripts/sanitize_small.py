@@ -40,3 +40,18 @@ _ = rf.stats.phi
 m = fca.m_step(rf.stats, fca.FcaParams(S0, v0), 0.0)
 fastfca.params_from_covariances(S0 + 0.1, v0)
 print("all ok", flush=True)
+
+# output-side tiles (statistics refresh / images: cp.async ring, staged stores, partial tiles),
+# initialisers, STFT, SDR and the device pipeline
+from paper_1805_09498_b200 import pipeline, scene  # noqa: E402
+
+for c64 in (True, False):
+    run(3, 3, 45, 50, c64=c64)   # F=45: one full and one partial 32-bin tile
+    run(2, 4, 33, 17, c64=c64)
+rng = np.random.default_rng(0)
+refs = rng.standard_normal((2, 2, 3000))
+for algo in ("fastfca", "fca"):
+    for init in ("oracle", "diffuse"):
+        pipeline.separate_once(pipeline.PipelineConfig(algorithm=algo, init=init, iterations=2, sources=2,
+                                                       frame_length=256, frame_shift=128), refs.sum(axis=0), refs)
+print("ok pipeline", flush=True)
