@@ -27,6 +27,24 @@
 
 namespace ffca {
 
+// Development probe (build with -DFFCA_PHASE_PROBE): per-phase clock64 cycle sums of threads 0
+// and 1 of the middle CTA, read back with ffca_debug_phase (loop_f32.cu).  Compiled out otherwise.
+#ifdef FFCA_PHASE_PROBE
+__device__ unsigned long long g_phase[16];
+#define FFCA_PROBE_INIT                                                       \
+  long long _pt = clock64();                                                  \
+  const bool _pr = (blockIdx.x == gridDim.x / 2) && threadIdx.x < 2;
+#define FFCA_PROBE(k)                                                                            \
+  if (_pr) {                                                                                     \
+    const long long _n = clock64();                                                              \
+    atomicAdd(&g_phase[(k) + 8 * threadIdx.x], (unsigned long long)(_n - _pt));                  \
+    _pt = _n;                                                                                    \
+  }
+#else
+#define FFCA_PROBE_INIT
+#define FFCA_PROBE(k)
+#endif
+
 
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -208,6 +226,30 @@ __device__ __forceinline__ void bin_reduce(const R (&vals)[V], double* wpart, do
   for (int k = 0; k < V2 / L; ++k)
     if (base + k < V) row[base + k] = double(buf[k]);
   bin_reduce_tail<G>(V, wpart, cpart, tot, C, VMAX, parity);
+}
+
+// Column c of the cofactor matrix of an I x I complex matrix A (row-major in shared memory,
+// I <= 3): out[x] = (-1)^(x+c) * minor(x, c), so that row c of A^-1 is out / det(A).  Elements are
+// read from shared memory as needed (no register copy of A).
+template <int I>
+__device__ __forceinline__ void adjugate_column(const double2* A, int c, double2 (&out)[I]) {
+  if constexpr (I == 1) {
+    out[0] = make_double2(1.0, 0.0);
+  } else if constexpr (I == 2) {
+    const double sg = (c == 0) ? 1.0 : -1.0;
+    const double2 a1 = A[2 + (1 - c)], a0 = A[1 - c];
+    out[0] = make_double2(sg * a1.x, sg * a1.y);
+    out[1] = make_double2(-sg * a0.x, -sg * a0.y);
+  } else {
+    const int c1 = c == 0 ? 1 : 0, c2 = c == 2 ? 1 : 2;
+#pragma unroll
+    for (int x = 0; x < 3; ++x) {
+      const int r1 = x == 0 ? 1 : 0, r2 = x == 2 ? 1 : 2;
+      const double2 p = cmul(A[r1 * 3 + c1], A[r2 * 3 + c2]), q = cmul(A[r1 * 3 + c2], A[r2 * 3 + c1]);
+      const double2 m = make_double2(p.x - q.x, p.y - q.y);
+      out[x] = ((x + c) & 1) ? make_double2(-m.x, -m.y) : m;
+    }
+  }
 }
 
 // Per-point work of one thread over its frames of one bin (registers only).
@@ -769,6 +811,7 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
   }
 
   // ======================= outer iterations =======================
+  FFCA_PROBE_INIT
   for (int it = 0; it < a.iters; ++it) {
     // ---------------- phase A: fused E/M sweep ----------------
     double llA = 0.0;
@@ -785,7 +828,9 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
         if (vf2) pw.template phaseA<false, true>(acc, vfl_b);
         else pw.template phaseA<false, false>(acc, vfl_b);
       }
+      FFCA_PROBE(0)
       bin_reduce<R, VA, G>(acc, wpart, cpart, tot, C, VMAX, parity);
+      FFCA_PROBE(1)
       if (rec && tid < G) llA = tot[tid * VMAX + VA - 1];
       // ---------------- lambda' per (bin, source) (fastfca.py:341-345) -------
       for (int t = tid; t < G * J; t += blockDim.x) {
@@ -808,6 +853,7 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
         }
       }
       __syncthreads();
+      FFCA_PROBE(2)
     }
 
     // ---------------- phase B: weighted covariances ----------------
@@ -859,6 +905,7 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
       for (int k = 0; k < NB + 1; ++k) acc[k] = R(0);
       if (rec && ch == 0) pw.template phaseB<true>(acc, ch);
       else pw.template phaseB<false>(acc, ch);
+      FFCA_PROBE(3)
       bin_reduce<R, NB + 1, G>(acc, wpart, cpart, tot, C, VMAX, parity);
       if (rec && ch == 0 && tid < G) llB = tot[tid * VMAX + NB];
       // keep this chunk of B in fp64 for the solve
@@ -870,13 +917,15 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
     }
     }
     __syncthreads();
+    FFCA_PROBE(4)
 
     // ---------------- solve: P^-1 and new columns (fastfca.py:359-370) --------
     if constexpr (I <= 4) {
-      // Thread (bin gg, s): s == 0 factors P (LU, partial pivoting) and
-      // publishes the factors; s = 1 + i factors B_i = L D L^H in registers.
-      // After one barrier every s >= 1 thread forms [P^-H]_i = conj(row i of
-      // P^-1) from the shared LU and solves B_i x = [P^-H]_i itself.
+      // Thread (bin gg, s = 1 + i) factors B_i = L D L^H in registers, forms
+      // [P^-H]_i = conj(row i of P^-1) and solves B_i x = [P^-H]_i itself.  Row i of
+      // P^-1 comes from the adjugate for I <= 3 (each thread alone, no divergent
+      // branch); for I = 4 thread s == 0 factors P (LU, partial pivoting) and
+      // publishes the factors to the s >= 1 threads of its warp.
       static_assert(G * (I + 1) <= 32, "the per-bin solver threads must be lanes of one warp");
       const int s = tid % (I + 1);
       const int gg = tid / (I + 1);
@@ -909,8 +958,47 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
           if (crank == 0) atomicOr(&a.status[b], ldl.ok ? ST_B_LOADED : ST_SINGULAR_B);
         }
       }
+      FFCA_PROBE(5)
 #pragma unroll 1
       for (int k = 0; k < a.K; ++k) {
+        if constexpr (I <= 3) {
+          // I <= 3: every solver thread forms its row of P^-1 from the adjugate (cofactors /
+          // det) -- no divergent LU thread and no publication step (measured: the LU thread
+          // and the LDL threads of one warp ran serially, 11 % of the iteration).  An exactly
+          // zero determinant flags SingularP, as an exactly zero LU pivot does for the
+          // structurally singular P the reference rejects (zero / repeated columns).
+          double2 z[I], det = make_double2(0.0, 0.0);
+          if (bact && s > 0) {
+            const double2* Pb = Pd + gg * I * I;
+            double2 c0[I];
+            adjugate_column<I>(Pb, s - 1, z);  // cofactors C[x][i]
+            adjugate_column<I>(Pb, 0, c0);     // cofactors C[x][0] for det
+#pragma unroll
+            for (int x = 0; x < I; ++x) det = cadd(det, cmul(Pb[x * I], c0[x]));
+          }
+          __syncwarp();  // every column is read before any thread writes its new one
+          if (bact && s > 0) {
+            const int i = s - 1;
+            if (det.x == 0.0 && det.y == 0.0) {
+              if (i == 0 && crank == 0) atomicOr(&a.status[b], ST_SINGULAR_P);
+            }
+            if (rec && k == 0 && i == 0) ldet[gg] = log(hypot(det.x, det.y));
+            const double2 rd = crecip(det);
+#pragma unroll
+            for (int x = 0; x < I; ++x) {  // [P^-H]_{x,i} = conj(P^-1_{i,x}) = conj(C[x][i] / det)
+              const double2 t = cmul(z[x], rd);
+              z[x] = make_double2(t.x, -t.y);
+            }
+            ldl.solve(z);
+#pragma unroll
+            for (int x = 0; x < I; ++x) {
+              Pd[(gg * I + x) * I + i] = z[x];
+              Pc[(gg * I + x) * I + i] = mk<C2, R>(R(z[x].x), R(z[x].y));
+            }
+          }
+          __syncwarp();
+          continue;
+        }
         if (bact && s == 0) {
           SmallLU<I> lu;
 #pragma unroll
@@ -933,6 +1021,7 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
         // LU publication (and, below, the column updates) -- the other warps go straight on
         // to the block barrier after the loop
         __syncwarp();
+        FFCA_PROBE(6)
         if (bact && s > 0) {
           const int i = s - 1;
           SmallLU<I> lu;
@@ -957,6 +1046,7 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
         __syncwarp();
       }
       __syncthreads();
+      FFCA_PROBE(7)
     } else {
       // I > 4: one group of 8 lanes per system (G == 1).  Group 0 inverts P,
       // groups 1..I invert B_i, all concurrently (Gauss-Jordan, row per lane);

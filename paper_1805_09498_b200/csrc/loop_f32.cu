@@ -40,3 +40,12 @@ LoopFn loop_kernel_f32(int I, int J, int G, bool res) {
 }
 
 }  // namespace ffca
+
+#ifdef FFCA_PHASE_PROBE
+extern "C" int ffca_debug_phase(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, ffca::g_phase, sizeof(unsigned long long) * 16);
+  unsigned long long z[16] = {};
+  cudaMemcpyToSymbol(ffca::g_phase, z, sizeof(z));
+  return 0;
+}
+#endif

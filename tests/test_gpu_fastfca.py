@@ -291,6 +291,29 @@ def test_singular_P_raises():
         fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=1)
 
 
+@pytest.mark.parametrize("dt", ["c128", "c64"])
+@pytest.mark.parametrize("how", ["zero_row", "zero_col", "repeated_col"])
+def test_singular_P_order3(dt, how):
+    # I = 3 rows of P^-1 come from the adjugate: an exactly zero determinant raises SingularP.
+    # Zero rows / columns raise in the reference too (zero LU pivot); for a repeated column the
+    # reference raises only when LAPACK's pivot happens to round to exactly zero (documented
+    # divergence).
+    y, P0, lam0, v0, _ = mixture(9, 3, 3, 4, 12)
+    y, P0, lam0, v0 = cast(dt, y, P0, lam0, v0)
+    if how == "zero_row":
+        P0[2, 1, :] = 0.0
+    elif how == "zero_col":
+        P0[2, :, 0] = 0.0
+    else:
+        P0[2, :, 2] = P0[2, :, 0]
+    with pytest.raises(errors.SingularP):
+        fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=1)
+    if how != "repeated_col":
+        with pytest.raises(ffr.OracleSingular):
+            ffr.run_fastfca(y.astype(np.complex128), P0.astype(np.complex128), lam0.astype(np.float64),
+                            v0.astype(np.float64), iterations=1)
+
+
 def test_zero_bin_raises_singular_weighted_covariance():
     y, P0, lam0, v0, _ = mixture(8, 2, 2, 3, 10)
     y[:, :, 2] = 0.0  # B_i = 0 for that bin, stays singular after trace loading
