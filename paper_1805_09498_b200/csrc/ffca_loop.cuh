@@ -908,15 +908,18 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
       FFCA_PROBE(3)
       bin_reduce<R, NB + 1, G>(acc, wpart, cpart, tot, C, VMAX, parity);
       if (rec && ch == 0 && tid < G) llB = tot[tid * VMAX + NB];
-      // keep this chunk of B in fp64 for the solve
-      const int nbc = (ch == NCH - 1) ? (I - ch * IC) * I * I : NB;
-      for (int t = tid; t < G * nbc; t += blockDim.x) {
-        const int gg = t / nbc, kk = t % nbc;
-        bst[gg * I * I * I + ch * NB + kk] = tot[gg * VMAX + kk];
+      // keep this chunk of B in fp64 for the solve (one chunk: the solve reads tot directly,
+      // which bin_reduce has already published to every thread)
+      if (NCH > 1) {
+        const int nbc = (ch == NCH - 1) ? (I - ch * IC) * I * I : NB;
+        for (int t = tid; t < G * nbc; t += blockDim.x) {
+          const int gg = t / nbc, kk = t % nbc;
+          bst[gg * I * I * I + ch * NB + kk] = tot[gg * VMAX + kk];
+        }
       }
     }
     }
-    __syncthreads();
+    if (Shape<I>::GROUPB || NCH > 1) __syncthreads();
     FFCA_PROBE(4)
 
     // ---------------- solve: P^-1 and new columns (fastfca.py:359-370) --------
@@ -936,7 +939,7 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
       SmallLDL<I> ldl;
       if (bact && s > 0) {
         const int i = s - 1;
-        const double* T = bst + gg * I * I * I + i * I * I;
+        const double* T = (NCH > 1 ? bst + gg * I * I * I : tot + gg * VMAX) + i * I * I;
         double2 B[I][I];
         double tr = 0.0;
         int kk = 0;
