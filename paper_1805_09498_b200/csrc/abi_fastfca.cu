@@ -62,7 +62,7 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
     p.NL = (N + C - 1) / C;
     p.threads = choose_threads(G, p.NL, I);
     p.resident = res;
-    LoopSmem L(I, J, G, p.NL, p.threads / 32, rsz, vf_mode, res, VMAX);
+    LoopSmem L(I, J, JM, G, p.NL, p.threads / 32, rsz, vf_mode, res, VMAX);
     p.L = L;
     p.smem = L.total;
     p.slab = L.slab;
@@ -78,7 +78,7 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
       fill(G, C, res != 0);
       if (nf == 4 && thr >= 64 && thr <= 256 && thr % 32 == 0 && (I <= 4 || thr >= 8 * (I + 1))) {
         p.threads = thr;
-        LoopSmem L(I, J, G, p.NL, thr / 32, rsz, vf_mode, res != 0, VMAX);
+        LoopSmem L(I, J, JM, G, p.NL, thr / 32, rsz, vf_mode, res != 0, VMAX);
         p.L = L;
         p.smem = L.total;
       }
@@ -89,15 +89,24 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
     fill(G, 1, true);
     if (p.slab <= kSlabBudget && p.smem <= smem_optin) return FFCA_OK;
   }
-  // I > 4: the per-iteration reductions (I^3 values) and solves dominate a
-  // cluster's small per-CTA frame ranges; one 256-thread CTA per bin streaming
-  // its slab from L2-resident global scratch is faster (measured on config 4).
+  // I > 4: 256-thread CTAs (8-lane point groups in phase B).  A bin whose interleaved slab
+  // fits the shared memory of one CTA or of a CTA pair / quad stays resident (one CTA per SM);
+  // larger clusters leave too few frames per CTA against the I^3-value reductions and solves,
+  // so longer bins stream their slab from L2-resident global scratch instead.
   if (I > 4) {
-    fill(1, 1, false);
-    p.threads = 256;
-    LoopSmem L(I, J, 1, p.NL, 8, rsz, vf_mode, false, VMAX);
-    p.L = L;
-    p.smem = L.total;
+    auto fill256 = [&](int C, bool res) {
+      fill(1, C, res);
+      p.threads = 256;
+      LoopSmem L(I, J, JM, 1, p.NL, 8, rsz, vf_mode, res, VMAX);
+      p.L = L;
+      p.smem = L.total;
+      p.slab = L.slab;
+    };
+    for (int C = 1; C <= 4 && C <= N; C <<= 1) {
+      fill256(C, true);
+      if (p.smem <= smem_optin) return FFCA_OK;
+    }
+    fill256(1, false);
     if (p.smem <= smem_optin) return FFCA_OK;
   }
   for (int C = 2; C <= 8; C <<= 1) {

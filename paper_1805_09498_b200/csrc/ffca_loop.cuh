@@ -50,40 +50,57 @@ __device__ unsigned long long g_phase[16];
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 __host__ __device__ constexpr int odd_up(int x) { return (x & 1) ? x : x + 1; }
 
-template <int I>
+// Slab record layout.  I <= 4: y records of odd(I) complex and separate v records of odd(J)
+// reals.  I > 4: one interleaved record per frame, I complex observations followed by the J
+// powers, odd(I + ceil(JM/2)) complex units long -- the odd stride keeps every lane-strided
+// access conflict free, and one record per frame lets a slab of 2 x 2000 frames of an 8-channel
+// bin fit the shared memory of a CTA pair (config 4).
+__host__ __device__ constexpr bool loop_interleaved(int I) { return I > 4; }
+__host__ __device__ constexpr int loop_rs(int I, int JM) {
+  return loop_interleaved(I) ? odd_up(I + (JM + 1) / 2) : odd_up(I);
+}
+__host__ __device__ constexpr int loop_js(int I, int JM, int J) { return loop_interleaved(I) ? 2 * loop_rs(I, JM) : odd_up(J); }
+
+template <int I, int JM>
 struct Shape {
   // i-chunking of the B accumulation: <= 64 accumulators per thread
   static constexpr int IC = (I * I * I <= 64) ? I : ((64 / (I * I)) > 0 ? (64 / (I * I)) : 1);
   static constexpr int NCH = (I + IC - 1) / IC;
   static constexpr int NB = IC * I * I;  // reals per chunk
   static constexpr bool PREG = I <= 4;   // keep P / lambda in registers
-  static constexpr int RS = odd_up(I);   // complex per slab record
-  // I > 4: the I^3 B accumulators are spread over groups of 8 lanes per point
+  static constexpr bool ILV = loop_interleaved(I);
+  static constexpr int RS = loop_rs(I, JM);  // complex units per slab record
+  // I > 4: phase B as a skinny GEMM, one accumulator unit (a complex off-diagonal entry or a
+  // pair of diagonal entries of B, for every i) per lane of a warp
   static constexpr bool GROUPB = I > 4;
-  static constexpr int NCX = I * (I - 1) / 2;        // complex off-diagonal entries
-  static constexpr int NSL = (NCX + 7) / 8;          // complex entries per lane
-  static constexpr int NVG = (1 + 2 * NSL) * I + 1;  // values per lane (+ likelihood)
+  static constexpr int NCX = I * (I - 1) / 2;   // complex off-diagonal entries
+  static constexpr int NU = NCX + (I + 1) / 2;  // accumulator units (<= 32 for I <= 8)
+  static constexpr int IWS = (I + 3) & ~3;      // reciprocal weights per frame in the warp buffer
 };
 
 template <int I, int JM>
 __host__ __device__ constexpr int loop_vmax() {
-  return Shape<I>::GROUPB
+  return Shape<I, JM>::GROUPB
              ? ((JM * (1 + I) + 1) > (I * I * I + 1) ? (JM * (1 + I) + 1) : (I * I * I + 1))
-             : ((JM * (1 + I) + 1) > (Shape<I>::NB + 1) ? (JM * (1 + I) + 1) : (Shape<I>::NB + 1));
+             : ((JM * (1 + I) + 1) > (Shape<I, JM>::NB + 1) ? (JM * (1 + I) + 1) : (Shape<I, JM>::NB + 1));
 }
 
-// Shared-memory carve-up; identical on host (sizing) and device.
+// Shared-memory carve-up; identical on host (sizing) and device.  The warp partials of the
+// reductions (wpart) and the solver workspace (M) are never live at the same time and share
+// one region.
 struct LoopSmem {
   size_t y, v, vf, Pc, Pd, Pinv, lamc, lamd, vfl, ldet, wpart, cpart, tot, bst, M, piv, rhs, total, slab;
   size_t ybytes, vbytes;
   LoopSmem() = default;
-  __host__ __device__ LoopSmem(int I, int J, int G, int NL, int W, int rsz, int vf_mode, bool resident,
+  __host__ __device__ LoopSmem(int I, int J, int JM, int G, int NL, int W, int rsz, int vf_mode, bool resident,
                                int VMAX) {
     size_t o = 0;
     const size_t csz = 2 * size_t(rsz);
-    ybytes = align16(size_t(NL) * G * odd_up(I) * csz);
-    vbytes = align16(size_t(NL) * G * odd_up(J) * rsz);
-    const size_t fs = vf_mode == 2 ? vbytes : 0;
+    const bool ilv = loop_interleaved(I);
+    const int JS = loop_js(I, JM, J);
+    ybytes = align16(size_t(NL) * G * loop_rs(I, JM) * csz);
+    vbytes = ilv ? 0 : align16(size_t(NL) * G * JS * rsz);
+    const size_t fs = vf_mode == 2 ? align16(size_t(NL) * G * JS * rsz) : 0;
     slab = ybytes + vbytes + fs;
     if (resident) {
       y = o; o += ybytes;
@@ -101,14 +118,19 @@ struct LoopSmem {
     lamd = o;  o += align16(size_t(G) * J * I * 8);
     vfl = o;   o += align16(size_t(G) * 8);
     ldet = o;  o += align16(size_t(G) * 8);
-    wpart = o; o += align16(size_t(W) * G * VMAX * 8);
     cpart = o; o += align16(size_t(2) * G * VMAX * 8);
     tot = o;   o += align16(size_t(G) * VMAX * 8);
-    bst = o;   o += align16(size_t(G) * I * I * I * 8);
+    bst = o;   // unused (the solves read the reduced sums in tot)
     {  // solver workspace: per-system matrices (I <= 4) or B_i^-1 + group rows (I > 4)
       const size_t m1 = size_t(G) * (I + 1) * I * I * 16, m2 = (size_t(I) * I * I + 2 * I * (I + 1)) * 16;
-      M = o;
-      o += align16(m1 > m2 ? m1 : m2);
+      size_t wp = align16(size_t(W) * G * VMAX * 8);
+      const size_t ms = align16(m1 > m2 ? m1 : m2);
+      if (ilv) {  // I > 4 phase B: per-warp buffers of 32 frames' reciprocal weights
+        const size_t wb = size_t(W) * 32 * ((I + 3) & ~3) * rsz;
+        wp = wp > wb ? wp : wb;
+      }
+      wpart = M = o;
+      o += wp > ms ? wp : ms;
     }
     rhs = o;   o += align16(size_t(G) * (I + 1) * I * 16);
     piv = o;   o += align16(size_t(G) * (I + 1) * I * 4);
@@ -252,12 +274,30 @@ __device__ __forceinline__ void adjugate_column(const double2* A, int c, double2
   }
 }
 
+// N consecutive reals from 16-byte aligned shared memory as 16-byte vector loads.
+template <int N>
+__device__ __forceinline__ void load_vec(const float* p, float (&o)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; i += 4) {
+    const float4 t = *(const float4*)(p + i);
+    o[i] = t.x; o[i + 1] = t.y; o[i + 2] = t.z; o[i + 3] = t.w;
+  }
+}
+template <int N>
+__device__ __forceinline__ void load_vec(const double* p, double (&o)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; i += 2) {
+    const double2 t = *(const double2*)(p + i);
+    o[i] = t.x; o[i + 1] = t.y;
+  }
+}
+
 // Per-point work of one thread over its frames of one bin (registers only).
 template <typename R, int I, int JM, int G>
 struct PointWork {
   using C2 = typename Cpx<R>::T;
-  static constexpr int IC = Shape<I>::IC, NB = Shape<I>::NB, RS = Shape<I>::RS;
-  static constexpr bool PREG = Shape<I>::PREG;
+  static constexpr int IC = Shape<I, JM>::IC, NB = Shape<I, JM>::NB, RS = Shape<I, JM>::RS;
+  static constexpr bool PREG = Shape<I, JM>::PREG;
   static constexpr int VA = JM * (1 + I) + 1;
 
   C2* ys;
@@ -430,6 +470,114 @@ struct PointWork {
     acc[VA - 1] = lacc;
   }
 
+  // Phase A for I > 4 (P stays in shared memory): two frames per step, so every P element
+  // read from shared memory feeds two points and the two points' dependent chains interleave;
+  // lambda is held in registers for the whole sweep.  Same arithmetic per point as phaseA.
+  template <bool REC, bool VF2>
+  __device__ __forceinline__ void phaseA2(R (&acc)[VA], const R vfl_b) {
+    R lam[JM][I];
+#pragma unroll
+    for (int j = 0; j < JM; ++j)
+#pragma unroll
+      for (int i = 0; i < I; ++i) lam[j][i] = (j < J) ? lamc[(g * J + j) * I + i] : R(0);
+    constexpr int IP = I / 2;
+    constexpr bool IODD = (I & 1) != 0;
+    R s0[JM], s1s[JM];
+    C2 s1p[JM][IP];  // (s1_j,2ip, s1_j,2ip+1) pairs: FFMA2
+    R lacc = R(0);
+#pragma unroll
+    for (int j = 0; j < JM; ++j) {
+      s0[j] = R(0);
+      s1s[j] = R(0);
+#pragma unroll
+      for (int ip = 0; ip < IP; ++ip) s1p[j][ip] = mk<C2, R>(R(0), R(0));
+    }
+    const int st = rstep;
+    const C2* yp = ys + rec0 * RS;
+    R* vp = vs + rec0 * JS;
+    const R* fp = vfs + rec0 * JS;
+#pragma unroll 1
+    for (int k = 0; k < npts; k += 2, yp += 2 * st * RS, vp += 2 * st * JS, fp += 2 * st * JS) {
+      const bool two = k + 1 < npts;
+      const int o1 = two ? st : 0;  // a lone last frame is computed twice, used once
+      C2 yv[2][I];
+      R vj[2][JM];
+      load_point(yp, vp, yv[0], vj[0]);
+      load_point(yp + o1 * RS, vp + o1 * JS, yv[1], vj[1]);
+      R q[2][I];
+#pragma unroll
+      for (int b = 0; b < I; ++b) {
+        C2 t0 = mk<C2, R>(R(0), R(0)), t1 = t0;
+#pragma unroll
+        for (int x = 0; x < I; ++x) {
+          const C2 pp = P(x, b);
+          t0 = fma2(yv[0][x], bc2<R>(pp.x), t0);
+          t0 = fma2(mk<C2, R>(yv[0][x].y, -yv[0][x].x), bc2<R>(pp.y), t0);
+          t1 = fma2(yv[1][x], bc2<R>(pp.x), t1);
+          t1 = fma2(mk<C2, R>(yv[1][x].y, -yv[1][x].x), bc2<R>(pp.y), t1);
+        }
+        q[0][b] = t0.x * t0.x + t0.y * t0.y;
+        q[1][b] = t1.x * t1.x + t1.y * t1.y;
+      }
+      R iw[2][I], d[2][I];
+#pragma unroll
+      for (int i = 0; i < I; ++i) {
+        C2 w2 = mk<C2, R>(R(0), R(0));  // (w of frame 0, w of frame 1)
+#pragma unroll
+        for (int j = 0; j < JM; ++j)
+          if (j < J) w2 = fma2(mk<C2, R>(vj[0][j], vj[1][j]), bc2<R>(lam[j][i]), w2);
+        const R w0 = fmax(w2.x, wfl), w1 = fmax(w2.y, wfl);
+        iw[0][i] = rcp_pt(w0);
+        iw[1][i] = rcp_pt(w1);
+        d[0][i] = fma(q[0][i], iw[0][i], R(-1)) * iw[0][i];
+        d[1][i] = fma(q[1][i], iw[1][i], R(-1)) * iw[1][i];
+        if constexpr (REC) {
+          lacc += flog(w0) + q[0][i] * iw[0][i];
+          if (two) lacc += flog(w1) + q[1][i] * iw[1][i];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < JM; ++j) {
+        if (j < J) {
+          C2 sd = mk<C2, R>(R(0), R(0));
+#pragma unroll
+          for (int i = 0; i < I; ++i) sd = fma2(bc2<R>(lam[j][i]), mk<C2, R>(d[0][i], d[1][i]), sd);
+          R fl0 = vfl_b, fl1 = vfl_b;
+          if constexpr (VF2) {
+            fl0 = fp[j];
+            fl1 = fp[o1 * JS + j];
+          }
+          const R v0 = vj[0][j], v1 = vj[1][j];
+          const R vn0 = fmax(fma(sd.x, (v0 * v0) * invI, v0), fl0);
+          const R vn1 = fmax(fma(sd.y, (v1 * v1) * invI, v1), fl1);
+          const R r0 = v0 * rcp_pt(vn0);
+          const R r1 = two ? v1 * rcp_pt(vn1) : R(0);
+          s0[j] += r0 + r1;
+          const R rv0 = r0 * v0, rv1 = r1 * v1;
+#pragma unroll
+          for (int ip = 0; ip < IP; ++ip) {
+            s1p[j][ip] = fma2(bc2<R>(rv0), mk<C2, R>(d[0][2 * ip], d[0][2 * ip + 1]), s1p[j][ip]);
+            s1p[j][ip] = fma2(bc2<R>(rv1), mk<C2, R>(d[1][2 * ip], d[1][2 * ip + 1]), s1p[j][ip]);
+          }
+          if constexpr (IODD) s1s[j] = fma(rv1, d[1][I - 1], fma(rv0, d[0][I - 1], s1s[j]));
+          vp[j] = vn0;
+          if (two) vp[o1 * JS + j] = vn1;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < JM; ++j) {
+      acc[j] = s0[j];
+#pragma unroll
+      for (int ip = 0; ip < IP; ++ip) {
+        acc[JM + j * I + 2 * ip] = s1p[j][ip].x;
+        acc[JM + j * I + 2 * ip + 1] = s1p[j][ip].y;
+      }
+      if constexpr (IODD) acc[JM + j * I + I - 1] = s1s[j];
+    }
+    acc[VA - 1] = lacc;
+  }
+
   // Phase B: weighted covariances (fastfca.py:352-358), I <= 4 (all i in one
   // pass); with REC also the likelihood at (P, v', lambda') (after-EM).
   // Off-diagonal outer-product entries y_x conj(y_y) are (re, im) pairs and
@@ -515,99 +663,82 @@ struct PointWork {
     acc[NB] = lacc;
   }
 
-  // Phase B for I > 4: lanes with the same (bin g, group q) cooperate on one
-  // point; lane position p = 0..7 owns the diagonal entry (p, p) and the
-  // complex entries c = p, p+8, ... of the packed lower triangle, for all i,
-  // so every product y_x conj(y_y) is formed once and each lane holds at most
-  // (1 + 2*NSL)*I accumulators.  Each lane forms 1/w_p and broadcasts it.
-  static constexpr int NSL = Shape<I>::NSL, NVG = Shape<I>::NVG;
+  // Phase B for I > 4 as a skinny GEMM over the frames: B_i[e] = sum_n Z_e(n) / w_i(n), with
+  // Z_e = y_a conj(y_b).  A warp walks chunks of 32 frames (chunk c of the CTA belongs to warp
+  // c % W): lane l first forms the I reciprocal weights of frame 32c + l (and, with REC, its
+  // likelihood terms) into the warp's buffer, then every lane accumulates its own unit -- one
+  // complex entry (ua > ub) or two diagonal entries (ua, ub) -- against all I weights of each
+  // frame: two y loads, one product and I FFMA2 per lane and frame, no cross-lane reduction.
+  // Frames past the bin's range get zero weights (their records are zero-filled or clamped).
   template <bool REC>
-  __device__ __forceinline__ void phaseB_group(R (&acc)[NVG], int NLr, bool active, const int (&cx)[NSL ? NSL : 1],
-                                               const int (&cy)[NSL ? NSL : 1]) const {
+  __device__ __forceinline__ void phaseB_entry(C2 (&ac)[I], R& lacc, int NLr, bool active, R* wbuf, int ua, int ub,
+                                               bool diag) const {
+    constexpr int IWS = Shape<I, JM>::IWS;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
-    constexpr int QW = 4 / G;  // point groups per bin per warp
-    const int p = (lane / G) % 8, q = lane / (8 * G);
-    const int start = warp * QW + q, stride = W * QW;
-    const int src0 = q * 8 * G + g;
-    // warp-uniform trip count (every lane must reach the shuffles); lanes whose
-    // point is out of range, or whose bin is padding, contribute nothing
-    const int trips = (NLr > warp * QW) ? (NLr - warp * QW + stride - 1) / stride : 0;
-    // pair accumulators: (re, im) of each owned complex entry per i (FFMA2)
-    C2 ac[NSL ? NSL : 1][I];
-    R ad[I];
-    R lacc = R(0);
+    R lam[JM][I];
 #pragma unroll
-    for (int i = 0; i < I; ++i) {
-      ad[i] = R(0);
+    for (int j = 0; j < JM; ++j)
 #pragma unroll
-      for (int s = 0; s < (NSL ? NSL : 1); ++s) ac[s][i] = mk<C2, R>(R(0), R(0));
-    }
-    bool own[NSL ? NSL : 1];
+      for (int i = 0; i < I; ++i) lam[j][i] = (j < J) ? lamc[j * I + i] : R(0);
 #pragma unroll
-    for (int s = 0; s < NSL; ++s) own[s] = p + 8 * s < Shape<I>::NCX;
+    for (int i = 0; i < I; ++i) ac[i] = mk<C2, R>(R(0), R(0));
+    const int nch = active ? (NLr + 31) / 32 : 0;
 #pragma unroll 1
-    for (int k = 0; k < trips; ++k) {
-      const int n = start + k * stride;
-      const bool valid = active && n < NLr;
-      const int nn = valid ? n : 0;
-      const C2* yp = ys + (nn * G + g) * RS;
-      const R* vp = vs + (nn * G + g) * JS;
-      if (gslab && n + PFD * stride < NLr && p < 2) {  // two lanes per point: its y and v records
-        const int np = n + PFD * stride;
-        if (p == 0) prefetch_l1(ys + (np * G + g) * RS);
-        else prefetch_l1(vs + (np * G + g) * JS);
-      }
-      R iw_own = R(0);
-      if (valid && p < I) {
-        R s = R(0);
+    for (int c = warp; c < nch; c += W) {
+      {  // reciprocal weights of frame 32c + lane
+        const int n = 32 * c + lane;
+        const bool ok = n < NLr;
+        const int nn = ok ? n : 0;
+        const R* vp = vs + nn * JS;
+        R vj[JM];
 #pragma unroll
-        for (int j = 0; j < JM; ++j)
-          if (j < J) s = fma(vp[j], Lam(j, p), s);
-        iw_own = rcp_pt(fmax(s, wfl));
-      }
-      R iw[I];
+        for (int j = 0; j < JM; ++j) vj[j] = (j < J) ? vp[j] : R(0);
+        R iw[IWS];
 #pragma unroll
-      for (int i = 0; i < I; ++i) iw[i] = __shfl_sync(FULL, iw_own, src0 + i * G);
-      if (valid && p < I) {
-        const C2 yd = yp[p];
-        const R dv = yd.x * yd.x + yd.y * yd.y;
+        for (int i = 0; i < IWS; ++i) iw[i] = R(0);
 #pragma unroll
-        for (int i = 0; i < I; ++i) ad[i] = fma(dv, iw[i], ad[i]);
-      }
+        for (int i = 0; i < I; ++i) {
+          R s = R(0);
 #pragma unroll
-      for (int s = 0; s < NSL; ++s) {
-        if (valid && own[s]) {
-          const C2 a = yp[cx[s]], b = yp[cy[s]];
-          // a conj(b) = b.x (a.x, a.y) + b.y (a.y, -a.x)
-          const C2 o = fma2(mk<C2, R>(a.y, -a.x), bc2<R>(b.y), fma2(a, bc2<R>(b.x), mk<C2, R>(R(0), R(0))));
-#pragma unroll
-          for (int i = 0; i < I; ++i) ac[s][i] = fma2(o, bc2<R>(iw[i]), ac[s][i]);
+          for (int j = 0; j < JM; ++j)
+            if (j < J) s = fma(vj[j], lam[j][i], s);
+          iw[i] = ok ? rcp_pt(fmax(s, wfl)) : R(0);
         }
-      }
-      if constexpr (REC) {
-        if (valid && p == 0) {
-          C2 yv[I];
+        if constexpr (REC) {
+          if (ok) {
+            C2 yv[I];
 #pragma unroll
-          for (int i = 0; i < I; ++i) yv[i] = yp[i];
-          R q2[I];
-          transform_q(yv, q2);
-          R l = R(0);
+            for (int i = 0; i < I; ++i) yv[i] = ys[nn * RS + i];
+            R q[I];
+            transform_q(yv, q);
 #pragma unroll
-          for (int i = 0; i < I; ++i) l += flog(R(1) / iw[i]) + q2[i] * iw[i];
-          lacc += l;
+            for (int i = 0; i < I; ++i) lacc += flog(R(1) / iw[i]) + q[i] * iw[i];
+          }
         }
-      }
-    }
+        R* wr = wbuf + lane * IWS;
 #pragma unroll
-    for (int i = 0; i < I; ++i) {
-      acc[i] = ad[i];
-#pragma unroll
-      for (int s = 0; s < NSL; ++s) {
-        acc[(1 + 2 * s) * I + i] = ac[s][i].x;
-        acc[(2 + 2 * s) * I + i] = ac[s][i].y;
+        for (int i = 0; i < IWS; i += 2) *(C2*)(wr + i) = mk<C2, R>(iw[i], iw[i + 1]);
       }
+      __syncwarp();
+      const int nf = min(32, NLr - 32 * c);
+      const C2* rec = ys + (32 * c) * RS;
+#pragma unroll 4
+      for (int f = 0; f < nf; ++f, rec += RS) {
+        const C2 ya = rec[ua], yb = rec[ub];
+        // complex unit: ya conj(yb) = yb.x (ya.x, ya.y) + yb.y (ya.y, -ya.x); diagonal pair: (|ya|^2, |yb|^2)
+        C2 z;
+        if (diag) {
+          z = mk<C2, R>(ya.x * ya.x + ya.y * ya.y, yb.x * yb.x + yb.y * yb.y);
+        } else {
+          z = fma2(mk<C2, R>(ya.y, -ya.x), bc2<R>(yb.y), fma2(ya, bc2<R>(yb.x), mk<C2, R>(R(0), R(0))));
+        }
+        R wv[IWS];
+        load_vec<IWS>(wbuf + f * IWS, wv);
+#pragma unroll
+        for (int i = 0; i < I; ++i) ac[i] = fma2(z, bc2<R>(wv[i]), ac[i]);
+      }
+      __syncwarp();
     }
-    acc[NVG - 1] = lacc;
   }
 
   // Likelihood partial sum_n,i ln w + q / w at the current state.
@@ -628,16 +759,16 @@ struct PointWork {
 };
 
 template <typename R, int I, int JT, int G, bool RES>
-__global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const LoopArgs a) {
+__global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffca_loop_kernel(const LoopArgs a) {
   using C2 = typename Cpx<R>::T;
   constexpr int JM = JT > 0 ? JT : 8;
-  constexpr int IC = Shape<I>::IC, NCH = Shape<I>::NCH, NB = Shape<I>::NB;
-  constexpr bool PREG = Shape<I>::PREG;
-  constexpr int RS = Shape<I>::RS;
+  constexpr int IC = Shape<I, JM>::IC, NCH = Shape<I, JM>::NCH, NB = Shape<I, JM>::NB;
+  constexpr bool PREG = Shape<I, JM>::PREG;
+  constexpr int RS = Shape<I, JM>::RS;
   constexpr int VMAX = loop_vmax<I, JM>();
   constexpr int VA = JM * (1 + I) + 1;
   const int J = JT > 0 ? JT : a.J;
-  const int JS = odd_up(J);
+  const int JS = loop_js(I, JM, J);
   const int C = a.C;
   const int tid = threadIdx.x;
   const int g = tid % G;
@@ -662,7 +793,7 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
 
   unsigned char* slab = resident ? smem : (unsigned char*)a.scratch + (long long)blockIdx.x * a.slab_bytes;
   C2* ys = (C2*)(slab + L.y);
-  R* vs = (R*)(slab + L.v);
+  R* vs = Shape<I, JM>::ILV ? (R*)(ys + I) : (R*)(slab + L.v);  // interleaved: v follows y in each record
   R* vfs = (R*)(slab + L.vf);
   C2* Pc = (C2*)(smem + L.Pc);
   double2* Pd = (double2*)(smem + L.Pd);
@@ -674,7 +805,6 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
   double* wpart = (double*)(smem + L.wpart);
   double* cpart = (double*)(smem + L.cpart);
   double* tot = (double*)(smem + L.tot);
-  double* bst = (double*)(smem + L.bst);
   double2* Msys = (double2*)(smem + L.M);
   double2* rhsv = (double2*)(smem + L.rhs);
   int* pivs = (int*)(smem + L.piv);
@@ -793,21 +923,24 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
   pw.g = g; pw.J = J; pw.JS = JS; pw.rec0 = rec0; pw.rstep = rstep; pw.npts = npts;
   pw.wfl = wfl; pw.invI = invI;
 
-  // complex off-diagonal entries (x, y < x) owned by this lane in group-mode phase B
-  int gcx[Shape<I>::NSL ? Shape<I>::NSL : 1], gcy[Shape<I>::NSL ? Shape<I>::NSL : 1];
-  if constexpr (Shape<I>::GROUPB) {
-    const int p = ((tid & 31) / G) % 8;
-#pragma unroll
-    for (int s = 0; s < Shape<I>::NSL; ++s) {
-      const int c = p + 8 * s;
+  // accumulator unit of this lane in the I > 4 phase B: a complex entry (x, y < x) of the packed
+  // lower triangle, or a pair of diagonal entries (2d, 2d + 1)
+  int bua = 0, bub = 0;
+  bool bdiag = false, bown = false;
+  if constexpr (Shape<I, JM>::GROUPB) {
+    const int u = tid & 31;
+    bown = u < Shape<I, JM>::NU;
+    if (u < Shape<I, JM>::NCX) {
       int x = 1;
-      while ((x + 1) * x / 2 <= c) ++x;
-      gcx[s] = x;
-      gcy[s] = c - x * (x - 1) / 2;
-      if (c >= Shape<I>::NCX) gcx[s] = gcy[s] = 0;
+      while ((x + 1) * x / 2 <= u) ++x;
+      bua = x;
+      bub = u - x * (x - 1) / 2;
+    } else if (bown) {
+      const int d = u - Shape<I, JM>::NCX;
+      bdiag = true;
+      bua = 2 * d;
+      bub = 2 * d + 1 < I ? 2 * d + 1 : 2 * d;
     }
-  } else {
-    gcx[0] = gcy[0] = 0;
   }
 
   // ======================= outer iterations =======================
@@ -821,12 +954,22 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
 #pragma unroll
       for (int k = 0; k < VA; ++k) acc[k] = R(0);
       const R vfl_b = R(vfl[g]);
-      if (rec) {
-        if (vf2) pw.template phaseA<true, true>(acc, vfl_b);
-        else pw.template phaseA<true, false>(acc, vfl_b);
+      if constexpr (PREG) {
+        if (rec) {
+          if (vf2) pw.template phaseA<true, true>(acc, vfl_b);
+          else pw.template phaseA<true, false>(acc, vfl_b);
+        } else {
+          if (vf2) pw.template phaseA<false, true>(acc, vfl_b);
+          else pw.template phaseA<false, false>(acc, vfl_b);
+        }
       } else {
-        if (vf2) pw.template phaseA<false, true>(acc, vfl_b);
-        else pw.template phaseA<false, false>(acc, vfl_b);
+        if (rec) {
+          if (vf2) pw.template phaseA2<true, true>(acc, vfl_b);
+          else pw.template phaseA2<true, false>(acc, vfl_b);
+        } else {
+          if (vf2) pw.template phaseA2<false, true>(acc, vfl_b);
+          else pw.template phaseA2<false, false>(acc, vfl_b);
+        }
       }
       FFCA_PROBE(0)
       bin_reduce<R, VA, G>(acc, wpart, cpart, tot, C, VMAX, parity);
@@ -859,45 +1002,37 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
     // ---------------- phase B: weighted covariances ----------------
     pw.load_PL();
     double llB = 0.0;
-    if constexpr (Shape<I>::GROUPB) {
-      constexpr int NSL = Shape<I>::NSL, NVG = Shape<I>::NVG;
-      R acc[NVG];
+    if constexpr (Shape<I, JM>::GROUPB) {
+      C2 bac[I];
+      R lacc = R(0);
+      R* wbuf = (R*)wpart + (tid >> 5) * 32 * Shape<I, JM>::IWS;  // free until the reduction below
+      if (rec) pw.template phaseB_entry<true>(bac, lacc, NLr, active, wbuf, bua, bub, bdiag);
+      else pw.template phaseB_entry<false>(bac, lacc, NLr, active, wbuf, bua, bub, bdiag);
+      FFCA_PROBE(3)
+      if (rec) lacc = warp_sum_seg(lacc, 1);
+      __syncthreads();  // every warp is done with its weight buffer (it aliases the partials)
+      {
+        double* wp = wpart + (tid >> 5) * VMAX;
+        if (bdiag) {
 #pragma unroll
-      for (int kk = 0; kk < NVG; ++kk) acc[kk] = R(0);
-      if (rec) pw.template phaseB_group<true>(acc, NLr, active, gcx, gcy);
-      else pw.template phaseB_group<false>(acc, NLr, active, gcx, gcy);
-      // reduce over the point groups of the warp (lanes differing in q only)
-      const int lane = tid & 31, warp = tid >> 5;
-      const int p = (lane / G) % 8, q = lane / (8 * G);
-#pragma unroll
-      for (int kk = 0; kk < NVG; ++kk) {
-#pragma unroll
-        for (int o = 16; o >= 8 * G; o >>= 1) acc[kk] += __shfl_xor_sync(FULL, acc[kk], o);
-      }
-      if (q == 0) {
-        double* wp = wpart + (warp * G + g) * VMAX;
-        if (p < I)
-#pragma unroll
-          for (int i = 0; i < I; ++i) wp[i * I * I + p * p] = double(acc[i]);
-#pragma unroll
-        for (int s = 0; s < NSL; ++s)
-          if (p + 8 * s < Shape<I>::NCX) {
-            const int e = gcx[s] * gcx[s] + 1 + 2 * gcy[s];
-#pragma unroll
-            for (int i = 0; i < I; ++i) {
-              wp[i * I * I + e] = double(acc[(1 + 2 * s) * I + i]);
-              wp[i * I * I + e + 1] = double(acc[(2 + 2 * s) * I + i]);
-            }
+          for (int i = 0; i < I; ++i) {
+            wp[i * I * I + bua * bua] = double(bac[i].x);
+            if (bub != bua) wp[i * I * I + bub * bub] = double(bac[i].y);
           }
-        if (p == 0) wp[I * I * I] = double(acc[NVG - 1]);
+        } else if (bown) {
+          const int e = bua * bua + 1 + 2 * bub;
+#pragma unroll
+          for (int i = 0; i < I; ++i) {
+            wp[i * I * I + e] = double(bac[i].x);
+            wp[i * I * I + e + 1] = double(bac[i].y);
+          }
+        }
+        if ((tid & 31) == 0) wp[I * I * I] = double(lacc);
       }
       bin_reduce_tail<G>(I * I * I + 1, wpart, cpart, tot, C, VMAX, parity);
       if (rec && tid < G) llB = tot[tid * VMAX + I * I * I];
-      for (int t = tid; t < G * I * I * I; t += blockDim.x) {
-        const int gg = t / (I * I * I), kk = t % (I * I * I);
-        bst[gg * I * I * I + kk] = tot[gg * VMAX + kk];
-      }
     } else {
+    static_assert(NCH == 1, "I <= 4 accumulates every B_i in one pass");
 #pragma unroll 1
     for (int ch = 0; ch < NCH; ++ch) {
       R acc[NB + 1];
@@ -908,18 +1043,8 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
       FFCA_PROBE(3)
       bin_reduce<R, NB + 1, G>(acc, wpart, cpart, tot, C, VMAX, parity);
       if (rec && ch == 0 && tid < G) llB = tot[tid * VMAX + NB];
-      // keep this chunk of B in fp64 for the solve (one chunk: the solve reads tot directly,
-      // which bin_reduce has already published to every thread)
-      if (NCH > 1) {
-        const int nbc = (ch == NCH - 1) ? (I - ch * IC) * I * I : NB;
-        for (int t = tid; t < G * nbc; t += blockDim.x) {
-          const int gg = t / nbc, kk = t % nbc;
-          bst[gg * I * I * I + ch * NB + kk] = tot[gg * VMAX + kk];
-        }
-      }
     }
     }
-    if (Shape<I>::GROUPB || NCH > 1) __syncthreads();
     FFCA_PROBE(4)
 
     // ---------------- solve: P^-1 and new columns (fastfca.py:359-370) --------
@@ -939,7 +1064,7 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
       SmallLDL<I> ldl;
       if (bact && s > 0) {
         const int i = s - 1;
-        const double* T = (NCH > 1 ? bst + gg * I * I * I : tot + gg * VMAX) + i * I * I;
+        const double* T = tot + gg * VMAX + i * I * I;  // the reduced sums, published by bin_reduce
         double2 B[I][I];
         double tr = 0.0;
         int kk = 0;
@@ -1051,64 +1176,66 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
       __syncthreads();
       FFCA_PROBE(7)
     } else {
-      // I > 4: one group of 8 lanes per system (G == 1).  Group 0 inverts P,
-      // groups 1..I invert B_i, all concurrently (Gauss-Jordan, row per lane);
-      // then group 1+i applies B_i^-1 to [P^-H]_i.
+      // I > 4: one group of 8 lanes per system (G == 1).  Group 0 inverts P while
+      // groups 1..I invert B_i (Gauss-Jordan, row per lane); then group 1+i applies
+      // B_i^-1 to [P^-H]_i.
       static_assert(G == 1, "I > 4 runs one bin per CTA");
       const int m = tid >> 3, r = tid & 7;
       const unsigned gmask = 0xFFu << (8 * ((tid >> 3) & 3));
       const bool bact = (m <= I) && active;
       double2* Binv = Msys;                         // I x I x I  (row-major per i)
       double2* srow = Msys + I * I * I + m * 2 * I;  // group scratch
-      if (m >= 1 && m <= I) {
-        const int i = m - 1;
-        const double* T = bst + i * I * I;
-        double tr = 0.0;
-#pragma unroll
-        for (int x = 0; x < I; ++x) tr += T[x * x] * invN;
-        for (int pass = 0; pass < 2; ++pass) {
-          double2 ar[I], er[I];
-#pragma unroll
-          for (int c = 0; c < I; ++c) {
-            er[c] = make_double2(c == r ? 1.0 : 0.0, 0.0);
-            if (r >= I) { ar[c] = make_double2(0.0, 0.0); continue; }
-            const int hi = r >= c ? r : c, lo = r >= c ? c : r;
-            if (hi == lo) ar[c] = make_double2(T[hi * hi] * invN + (pass ? 1e-10 * tr : 0.0), 0.0);
-            else {
-              const double re = T[hi * hi + 1 + 2 * lo] * invN, im = T[hi * hi + 2 + 2 * lo] * invN;
-              ar[c] = make_double2(re, r >= c ? im : -im);
-            }
-          }
-          int krow;
-          double ld;
-          const bool ok = gj_group<I, false>(ar, er, r, gmask, srow, krow, ld);
-          if (ok || pass == 1) {
-            if (r < I)
-#pragma unroll
-              for (int c = 0; c < I; ++c) Binv[(i * I + krow) * I + c] = er[c];
-            if (pass == 1 && r == 0 && bact && crank == 0) atomicOr(&a.status[group], ok ? ST_B_LOADED : ST_SINGULAR_B);
-            break;
-          }
-        }
-      }
 #pragma unroll 1
       for (int k = 0; k < a.K; ++k) {
-        if (m == 0) {
-          double2 ar[I], er[I];
+        // group 0 inverts P; at k == 0 groups 1..I invert B_i (B does not depend on P) in
+        // the same pass -- every group of a warp runs the same gj_group call, converged
+        if (m == 0 || (k == 0 && m <= I)) {
+          const int i = m - 1;
+          const double* T = tot + (m > 0 ? i : 0) * I * I;
+          double tr = 0.0;
+          if (m > 0) {
 #pragma unroll
-          for (int c = 0; c < I; ++c) {
-            ar[c] = r < I ? Pd[r * I + c] : make_double2(0.0, 0.0);
-            er[c] = make_double2(c == r ? 1.0 : 0.0, 0.0);
+            for (int x = 0; x < I; ++x) tr += T[x * x] * invN;
           }
-          int krow;
-          double ld = 0.0;
-          const bool ok = (rec && k == 0) ? gj_group<I, true>(ar, er, r, gmask, srow, krow, ld)
-                                          : gj_group<I, false>(ar, er, r, gmask, srow, krow, ld);
-          if (!ok && r == 0 && bact && crank == 0) atomicOr(&a.status[group], ST_SINGULAR_P);
-          if (k == 0 && r == 0) ldet[0] = ld;
-          if (r < I)
+#pragma unroll 1
+          for (int pass = 0; pass < 2; ++pass) {
+            double2 ar[I], er[I];
 #pragma unroll
-            for (int c = 0; c < I; ++c) Pinv[krow * I + c] = er[c];
+            for (int c = 0; c < I; ++c) {
+              er[c] = make_double2(c == r ? 1.0 : 0.0, 0.0);
+              if (r >= I) {
+                ar[c] = make_double2(0.0, 0.0);
+              } else if (m == 0) {
+                ar[c] = Pd[r * I + c];
+              } else {
+                const int hi = r >= c ? r : c, lo = r >= c ? c : r;
+                if (hi == lo) ar[c] = make_double2(T[hi * hi] * invN + (pass ? 1e-10 * tr : 0.0), 0.0);
+                else {
+                  const double re = T[hi * hi + 1 + 2 * lo] * invN, im = T[hi * hi + 2 + 2 * lo] * invN;
+                  ar[c] = make_double2(re, r >= c ? im : -im);
+                }
+              }
+            }
+            int krow;
+            double ld = 0.0;
+            const bool ok = (rec && k == 0) ? gj_group<I, true>(ar, er, r, gmask, srow, krow, ld)
+                                            : gj_group<I, false>(ar, er, r, gmask, srow, krow, ld);
+            if (m == 0) {
+              if (!ok && r == 0 && bact && crank == 0) atomicOr(&a.status[group], ST_SINGULAR_P);
+              if (k == 0 && r == 0) ldet[0] = ld;
+              if (r < I)
+#pragma unroll
+                for (int c = 0; c < I; ++c) Pinv[krow * I + c] = er[c];
+              break;
+            }
+            if (ok || pass == 1) {  // one trace-loaded retry (fastfca.py:184-194)
+              if (r < I)
+#pragma unroll
+                for (int c = 0; c < I; ++c) Binv[(i * I + krow) * I + c] = er[c];
+              if (pass == 1 && r == 0 && bact && crank == 0) atomicOr(&a.status[group], ok ? ST_B_LOADED : ST_SINGULAR_B);
+              break;
+            }
+          }
         }
         __syncthreads();
         if (m >= 1 && m <= I && r < I) {
@@ -1125,6 +1252,7 @@ __global__ void __launch_bounds__(256, (I == 4 ? 1 : 2)) ffca_loop_kernel(const 
         }
         __syncthreads();
       }
+      FFCA_PROBE(7)
     }
     if (rec && tid < G) {
       const long long b = group * G + tid;
