@@ -41,7 +41,7 @@ static int choose_threads(int G, int NL, int I) {
   const int per_bin = (NL + 3) / 4;  // ~4 frames per thread per pass (capped at 256 threads)
   int t = G * per_bin;
   t = (t + 31) / 32 * 32;
-  const int tmin = I > 4 ? (8 * (I + 1) + 31) / 32 * 32 : 64;  // I > 4: 8-lane solver groups
+  const int tmin = I > 4 ? (8 * (loop_pgroup(I) + 1) + 31) / 32 * 32 : 64;  // I > 4: 8-lane solver groups
   if (t < tmin) t = tmin;
   // I >= 4 instantiations use up to 255 registers: 128-thread CTAs keep two per SM
   const int tmax = I >= 4 ? 128 : 256;
@@ -76,7 +76,7 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
     if (nf >= 3 && (G == 1 || G == G0 || (G == 2 && G0 == 4)) && (G == 1 || res) && C >= 1 && C <= 16 && (C & (C - 1)) == 0 && C <= N &&
         (C == 1 || G == 1)) {
       fill(G, C, res != 0);
-      if (nf == 4 && thr >= 64 && thr <= 256 && thr % 32 == 0 && (I <= 4 || thr >= 8 * (I + 1))) {
+      if (nf == 4 && thr >= 64 && thr <= 256 && thr % 32 == 0 && (I <= 4 || thr >= 8 * (loop_pgroup(I) + 1))) {
         p.threads = thr;
         LoopSmem L(I, J, JM, G, p.NL, thr / 32, rsz, vf_mode, res != 0, VMAX);
         p.L = L;

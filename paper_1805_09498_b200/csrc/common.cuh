@@ -413,7 +413,11 @@ __device__ __forceinline__ double2 crecip_fast(const double2 z) {
   return crecip(z);
 }
 
-template <int I, bool LOGDET>
+// PIVOT = false (Hermitian positive definite A, whose Schur complements stay HPD): row k is
+// the pivot of step k, no search; a pivot that is not > 0 in magnitude flags failure, like a
+// failed LDL^H.  The step loop stays rolled (instruction-cache footprint); column k of the
+// lane's row is picked with selects so a[] / e[] stay in registers.
+template <int I, bool LOGDET, bool PIVOT = true>
 __device__ __forceinline__ bool gj_group(double2 (&a)[I], double2 (&e)[I], int r, unsigned gmask, double2* srow,
                                          int& k_of_row, double& logabsdet) {
   bool used = r >= I;
@@ -422,18 +426,28 @@ __device__ __forceinline__ bool gj_group(double2 (&a)[I], double2 (&e)[I], int r
   k_of_row = -1;
 #pragma unroll 1
   for (int k = 0; k < I; ++k) {
-    double best = used ? -1.0 : cabs1(a[k]);
-    int who = r;
+    double2 ak = a[0];
 #pragma unroll
-    for (int o = 1; o < 8; o <<= 1) {
-      const double ob = __shfl_xor_sync(gmask, best, o);
-      const int ow = __shfl_xor_sync(gmask, who, o);
-      if (ob > best || (ob == best && ow < who)) { best = ob; who = ow; }
+    for (int c = 1; c < I; ++c)
+      if (c == k) ak = a[c];
+    double best;
+    int who = r;
+    if constexpr (PIVOT) {
+      best = used ? -1.0 : cabs1(ak);
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        const double ob = __shfl_xor_sync(gmask, best, o);
+        const int ow = __shfl_xor_sync(gmask, who, o);
+        if (ob > best || (ob == best && ow < who)) { best = ob; who = ow; }
+      }
+    } else {
+      who = k;
+      best = __shfl_sync(gmask, cabs1(ak), k, 8);
     }
     const bool piv = (who == r);
     if (!(best > 0.0)) ok = false;  // exactly zero (or no) pivot
     if (piv) {
-      const double2 d = a[k];
+      const double2 d = ak;
       if (LOGDET) logabsdet += log(hypot(d.x, d.y));
       const double2 inv = crecip_fast(d);
 #pragma unroll
@@ -448,7 +462,7 @@ __device__ __forceinline__ bool gj_group(double2 (&a)[I], double2 (&e)[I], int r
     }
     __syncwarp(gmask);
     if (!piv && r < I) {
-      const double2 f = a[k];
+      const double2 f = ak;
 #pragma unroll
       for (int c = 0; c < I; ++c) {
         const double2 pa = srow[c], pe = srow[I + c];

@@ -60,6 +60,9 @@ __host__ __device__ constexpr int loop_rs(int I, int JM) {
   return loop_interleaved(I) ? odd_up(I + (JM + 1) / 2) : odd_up(I);
 }
 __host__ __device__ constexpr int loop_js(int I, int JM, int J) { return loop_interleaved(I) ? 2 * loop_rs(I, JM) : odd_up(J); }
+// I > 4 solve: the 8-lane group that inverts P is the first group of the warp after the I
+// groups of the B_i (so it never shares a warp with them); the CTA needs 8 (mP + 1) threads.
+__host__ __device__ constexpr int loop_pgroup(int I) { return (I + 3) / 4 * 4; }
 
 template <int I, int JM>
 struct Shape {
@@ -122,7 +125,7 @@ struct LoopSmem {
     tot = o;   o += align16(size_t(G) * VMAX * 8);
     bst = o;   // unused (the solves read the reduced sums in tot)
     {  // solver workspace: per-system matrices (I <= 4) or B_i^-1 + group rows (I > 4)
-      const size_t m1 = size_t(G) * (I + 1) * I * I * 16, m2 = (size_t(I) * I * I + 2 * I * (I + 1)) * 16;
+      const size_t m1 = size_t(G) * (I + 1) * I * I * 16, m2 = (size_t(I) * I * I + 2 * I * (loop_pgroup(I) + 1)) * 16;
       size_t wp = align16(size_t(W) * G * VMAX * 8);
       const size_t ms = align16(m1 > m2 ? m1 : m2);
       if (ilv) {  // I > 4 phase B: per-warp buffers of 32 frames' reciprocal weights
@@ -1176,27 +1179,40 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
       __syncthreads();
       FFCA_PROBE(7)
     } else {
-      // I > 4: one group of 8 lanes per system (G == 1).  Group 0 inverts P while
-      // groups 1..I invert B_i (Gauss-Jordan, row per lane); then group 1+i applies
-      // B_i^-1 to [P^-H]_i.
+      // I > 4: one group of 8 lanes per system (G == 1), row per lane (Gauss-Jordan).  Groups
+      // 0..I-1 invert B_i (Hermitian positive definite: no pivot search) while group mP -- the
+      // first group of the next warp, so the two paths never share a warp -- inverts P with
+      // partial pivoting; then group i applies B_i^-1 to [P^-H]_i.  B does not depend on P, so
+      // for K > 1 only the P inversion repeats.
       static_assert(G == 1, "I > 4 runs one bin per CTA");
+      constexpr int mP = loop_pgroup(I);
       const int m = tid >> 3, r = tid & 7;
       const unsigned gmask = 0xFFu << (8 * ((tid >> 3) & 3));
-      const bool bact = (m <= I) && active;
       double2* Binv = Msys;                         // I x I x I  (row-major per i)
       double2* srow = Msys + I * I * I + m * 2 * I;  // group scratch
 #pragma unroll 1
       for (int k = 0; k < a.K; ++k) {
-        // group 0 inverts P; at k == 0 groups 1..I invert B_i (B does not depend on P) in
-        // the same pass -- every group of a warp runs the same gj_group call, converged
-        if (m == 0 || (k == 0 && m <= I)) {
-          const int i = m - 1;
-          const double* T = tot + (m > 0 ? i : 0) * I * I;
-          double tr = 0.0;
-          if (m > 0) {
+        if (m == mP) {
+          double2 ar[I], er[I];
 #pragma unroll
-            for (int x = 0; x < I; ++x) tr += T[x * x] * invN;
+          for (int c = 0; c < I; ++c) {
+            er[c] = make_double2(c == r ? 1.0 : 0.0, 0.0);
+            ar[c] = r < I ? Pd[r * I + c] : make_double2(0.0, 0.0);
           }
+          int krow;
+          double ld = 0.0;
+          const bool ok = (rec && k == 0) ? gj_group<I, true>(ar, er, r, gmask, srow, krow, ld)
+                                          : gj_group<I, false>(ar, er, r, gmask, srow, krow, ld);
+          if (!ok && r == 0 && active && crank == 0) atomicOr(&a.status[group], ST_SINGULAR_P);
+          if (k == 0 && r == 0) ldet[0] = ld;
+          if (r < I)
+#pragma unroll
+            for (int c = 0; c < I; ++c) Pinv[krow * I + c] = er[c];
+        } else if (k == 0 && m < I) {
+          const double* T = tot + m * I * I;
+          double tr = 0.0;
+#pragma unroll
+          for (int x = 0; x < I; ++x) tr += T[x * x] * invN;
 #pragma unroll 1
           for (int pass = 0; pass < 2; ++pass) {
             double2 ar[I], er[I];
@@ -1205,8 +1221,6 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
               er[c] = make_double2(c == r ? 1.0 : 0.0, 0.0);
               if (r >= I) {
                 ar[c] = make_double2(0.0, 0.0);
-              } else if (m == 0) {
-                ar[c] = Pd[r * I + c];
               } else {
                 const int hi = r >= c ? r : c, lo = r >= c ? c : r;
                 if (hi == lo) ar[c] = make_double2(T[hi * hi] * invN + (pass ? 1e-10 * tr : 0.0), 0.0);
@@ -1218,28 +1232,19 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
             }
             int krow;
             double ld = 0.0;
-            const bool ok = (rec && k == 0) ? gj_group<I, true>(ar, er, r, gmask, srow, krow, ld)
-                                            : gj_group<I, false>(ar, er, r, gmask, srow, krow, ld);
-            if (m == 0) {
-              if (!ok && r == 0 && bact && crank == 0) atomicOr(&a.status[group], ST_SINGULAR_P);
-              if (k == 0 && r == 0) ldet[0] = ld;
-              if (r < I)
-#pragma unroll
-                for (int c = 0; c < I; ++c) Pinv[krow * I + c] = er[c];
-              break;
-            }
+            const bool ok = gj_group<I, false, false>(ar, er, r, gmask, srow, krow, ld);
             if (ok || pass == 1) {  // one trace-loaded retry (fastfca.py:184-194)
               if (r < I)
 #pragma unroll
-                for (int c = 0; c < I; ++c) Binv[(i * I + krow) * I + c] = er[c];
-              if (pass == 1 && r == 0 && bact && crank == 0) atomicOr(&a.status[group], ok ? ST_B_LOADED : ST_SINGULAR_B);
+                for (int c = 0; c < I; ++c) Binv[(m * I + krow) * I + c] = er[c];
+              if (pass == 1 && r == 0 && active && crank == 0) atomicOr(&a.status[group], ok ? ST_B_LOADED : ST_SINGULAR_B);
               break;
             }
           }
         }
         __syncthreads();
-        if (m >= 1 && m <= I && r < I) {
-          const int i = m - 1;
+        if (m < I && r < I) {
+          const int i = m;
           double2 x = make_double2(0.0, 0.0);
 #pragma unroll
           for (int c = 0; c < I; ++c) {  // (B_i^-1)_{r,c} conj(P^-1_{i,c})
