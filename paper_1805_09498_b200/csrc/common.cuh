@@ -394,6 +394,68 @@ struct SmallLDL {
   }
 };
 
+// L D L^H of a Hermitian positive definite matrix held by one thread as its packed lower
+// triangle (row-major, b[r(r+1)/2 + c], c <= r) -- half the registers of SmallLDL's square
+// arrays, for I up to 8.  In place: b[(r,c)] becomes l_rc (c < r) and b[(k,k)] = (1/d_k, d_k).
+// The failure criterion is SmallLDL's (an exactly zero d_k).
+template <int I>
+struct PackedLDL {
+  static constexpr int NP = I * (I + 1) / 2;
+  __host__ __device__ static constexpr int id(int r, int c) { return r * (r + 1) / 2 + c; }
+  __device__ __forceinline__ static bool factor(double2 (&b)[NP]) {
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < I; ++k) {
+      double dk = b[id(k, k)].x;
+#pragma unroll
+      for (int c = 0; c < k; ++c) {
+        const double2 l = b[id(k, c)];
+        dk -= (l.x * l.x + l.y * l.y) * b[id(c, c)].y;
+      }
+      if (dk == 0.0) ok = false;
+      const double rk = (dk != 0.0) ? rcp(dk) : 0.0;
+      b[id(k, k)] = make_double2(rk, dk);
+#pragma unroll
+      for (int r = k + 1; r < I; ++r) {
+        double2 acc = b[id(r, k)];
+#pragma unroll
+        for (int c = 0; c < k; ++c) {  // acc -= l_rc d_c conj(l_kc)
+          const double2 lr = b[id(r, c)], lk = b[id(k, c)];
+          const double dc = b[id(c, c)].y;
+          acc.x -= (lr.x * lk.x + lr.y * lk.y) * dc;
+          acc.y -= (lr.y * lk.x - lr.x * lk.y) * dc;
+        }
+        b[id(r, k)] = make_double2(acc.x * rk, acc.y * rk);
+      }
+    }
+    return ok;
+  }
+  // x <- (L D L^H)^-1 x with the factor in (shared) memory
+  __device__ __forceinline__ static void solve(const double2* L, double2 (&x)[I]) {
+#pragma unroll
+    for (int r = 1; r < I; ++r)
+#pragma unroll
+      for (int c = 0; c < r; ++c) {
+        const double2 lv = L[id(r, c)];
+        x[r].x -= lv.x * x[c].x - lv.y * x[c].y;
+        x[r].y -= lv.x * x[c].y + lv.y * x[c].x;
+      }
+#pragma unroll
+    for (int r = 0; r < I; ++r) {
+      const double rd = L[id(r, r)].x;
+      x[r] = make_double2(x[r].x * rd, x[r].y * rd);
+    }
+#pragma unroll
+    for (int r = I - 1; r >= 0; --r)
+#pragma unroll
+      for (int c = r + 1; c < I; ++c) {  // (L^H)_{r,c} = conj(l_cr)
+        const double2 lv = L[id(c, r)];
+        x[r].x -= lv.x * x[c].x + lv.y * x[c].y;
+        x[r].y -= lv.x * x[c].y - lv.y * x[c].x;
+      }
+  }
+};
+
 // ------------------------------------------------------------------------
 // Gauss-Jordan elimination with partial pivoting on [A | E] by a group of 8
 // consecutive lanes; lane r < I owns row r (fp64, registers).  The pivot at
@@ -430,47 +492,47 @@ __device__ __forceinline__ bool gj_group(double2 (&a)[I], double2 (&e)[I], int r
 #pragma unroll
     for (int c = 1; c < I; ++c)
       if (c == k) ak = a[c];
-    double best;
-    int who = r;
+    int who = k;
     if constexpr (PIVOT) {
-      best = used ? -1.0 : cabs1(ak);
-#pragma unroll
-      for (int o = 1; o < 8; o <<= 1) {
-        const double ob = __shfl_xor_sync(gmask, best, o);
-        const int ow = __shfl_xor_sync(gmask, who, o);
-        if (ob > best || (ob == best && ow < who)) { best = ob; who = ow; }
-      }
-    } else {
-      who = k;
-      best = __shfl_sync(gmask, cabs1(ak), k, 8);
+      // max of |re|+|im| over the unused rows, lowest lane on ties, as three group-wide integer
+      // reductions on the (non-negative) double's bit pattern: high word (+1, so an unused row
+      // with an exactly zero entry still beats the used rows' 0), then low word, then lane
+      const double best = cabs1(ak);
+      const unsigned hi = used ? 0u : unsigned(__double2hiint(best)) + 1u;
+      const unsigned lo = unsigned(__double2loint(best));
+      const unsigned mh = __reduce_max_sync(gmask, hi);
+      const unsigned ml = __reduce_max_sync(gmask, hi == mh ? lo : 0u);
+      who = int(__reduce_min_sync(gmask, (hi == mh && lo == ml) ? unsigned(r) : 8u));
+      if (mh <= 1u && ml == 0u) ok = false;  // exactly zero (or no) pivot
     }
     const bool piv = (who == r);
-    if (!(best > 0.0)) ok = false;  // exactly zero (or no) pivot
     if (piv) {
-      const double2 d = ak;
-      if (LOGDET) logabsdet += log(hypot(d.x, d.y));
-      const double2 inv = crecip_fast(d);
 #pragma unroll
       for (int c = 0; c < I; ++c) {
-        a[c] = cmul(a[c], inv);
-        e[c] = cmul(e[c], inv);
         srow[c] = a[c];
         srow[I + c] = e[c];
       }
-      used = true;
-      k_of_row = k;
     }
     __syncwarp(gmask);
-    if (!piv && r < I) {
-      const double2 f = ak;
+    // every lane reads the unscaled pivot row and forms the same reciprocal; the pivot lane
+    // scales its row, the others subtract (a_k / pivot) times it -- one uniform update
+    const double2 d = srow[k];
+    if constexpr (!PIVOT) {
+      if (!(cabs1(d) > 0.0)) ok = false;
+    }
+    const double2 inv = crecip_fast(d);
+    if (LOGDET && piv) logabsdet += log(hypot(d.x, d.y));
+    const double2 f = cmul(ak, inv);
+    const double2 coef = piv ? inv : make_double2(-f.x, -f.y);
 #pragma unroll
-      for (int c = 0; c < I; ++c) {
-        const double2 pa = srow[c], pe = srow[I + c];
-        a[c].x -= f.x * pa.x - f.y * pa.y;
-        a[c].y -= f.x * pa.y + f.y * pa.x;
-        e[c].x -= f.x * pe.x - f.y * pe.y;
-        e[c].y -= f.x * pe.y + f.y * pe.x;
-      }
+    for (int c = 0; c < I; ++c) {
+      const double2 ta = cmul(coef, srow[c]), te = cmul(coef, srow[I + c]);
+      a[c] = piv ? ta : make_double2(a[c].x + ta.x, a[c].y + ta.y);
+      e[c] = piv ? te : make_double2(e[c].x + te.x, e[c].y + te.y);
+    }
+    if (piv) {
+      used = true;
+      k_of_row = k;
     }
     __syncwarp(gmask);
   }

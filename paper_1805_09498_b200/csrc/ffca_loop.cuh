@@ -30,14 +30,17 @@ namespace ffca {
 // Development probe (build with -DFFCA_PHASE_PROBE): per-phase clock64 cycle sums of threads 0
 // and 1 of the middle CTA, read back with ffca_debug_phase (loop_f32.cu).  Compiled out otherwise.
 #ifdef FFCA_PHASE_PROBE
+#ifndef FFCA_PROBE_T1
+#define FFCA_PROBE_T1 1  // second probed thread (e.g. 64: the P group of the I > 4 solve)
+#endif
 __device__ unsigned long long g_phase[16];
 #define FFCA_PROBE_INIT                                                       \
   long long _pt = clock64();                                                  \
-  const bool _pr = (blockIdx.x == gridDim.x / 2) && threadIdx.x < 2;
+  const bool _pr = (blockIdx.x == gridDim.x / 2) && (threadIdx.x == 0 || threadIdx.x == FFCA_PROBE_T1);
 #define FFCA_PROBE(k)                                                                            \
   if (_pr) {                                                                                     \
     const long long _n = clock64();                                                              \
-    atomicAdd(&g_phase[(k) + 8 * threadIdx.x], (unsigned long long)(_n - _pt));                  \
+    atomicAdd(&g_phase[(k) + 8 * (threadIdx.x != 0)], (unsigned long long)(_n - _pt));           \
     _pt = _n;                                                                                    \
   }
 #else
@@ -675,9 +678,9 @@ struct PointWork {
   // Frames past the bin's range get zero weights (their records are zero-filled or clamped).
   template <bool REC>
   __device__ __forceinline__ void phaseB_entry(C2 (&ac)[I], R& lacc, int NLr, bool active, R* wbuf, int ua, int ub,
-                                               bool diag) const {
+                                               bool diag, int warp, int W) const {
     constexpr int IWS = Shape<I, JM>::IWS;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31;
     R lam[JM][I];
 #pragma unroll
     for (int j = 0; j < JM; ++j)
@@ -760,6 +763,29 @@ struct PointWork {
     }
   }
 };
+
+// P^-1 by the 8 lanes r = 0..7 of one group (row per lane, Gauss-Jordan with partial pivoting,
+// numpy.linalg.inv's pivot order) into Pinv (row-major); with rec, log|det P| into ldet[0].
+template <int I>
+__device__ __forceinline__ void invert_P_group(const double2* Pd, double2* Pinv, double2* srow, int r, bool rec,
+                                               double* ldet, int* status, long long group, bool report) {
+  const unsigned gmask = 0xFFu << (8 * ((threadIdx.x >> 3) & 3));
+  double2 ar[I], er[I];
+#pragma unroll
+  for (int c = 0; c < I; ++c) {
+    er[c] = make_double2(c == r ? 1.0 : 0.0, 0.0);
+    ar[c] = r < I ? Pd[r * I + c] : make_double2(0.0, 0.0);
+  }
+  int krow;
+  double ld = 0.0;
+  const bool ok = rec ? gj_group<I, true>(ar, er, r, gmask, srow, krow, ld)
+                      : gj_group<I, false>(ar, er, r, gmask, srow, krow, ld);
+  if (!ok && r == 0 && report) atomicOr(&status[group], ST_SINGULAR_P);
+  if (rec && r == 0) ldet[0] = ld;
+  if (r < I)
+#pragma unroll
+    for (int c = 0; c < I; ++c) Pinv[krow * I + c] = er[c];
+}
 
 template <typename R, int I, int JT, int G, bool RES>
 __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffca_loop_kernel(const LoopArgs a) {
@@ -1006,11 +1032,22 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
     pw.load_PL();
     double llB = 0.0;
     if constexpr (Shape<I, JM>::GROUPB) {
+      // The last warp inverts P meanwhile (8-lane Gauss-Jordan, partial pivoting: P does not
+      // change before the solve), so P^-1 is off the per-iteration critical path; the other
+      // W - 1 warps share the frames.
       C2 bac[I];
+#pragma unroll
+      for (int i = 0; i < I; ++i) bac[i] = mk<C2, R>(R(0), R(0));
       R lacc = R(0);
-      R* wbuf = (R*)wpart + (tid >> 5) * 32 * Shape<I, JM>::IWS;  // free until the reduction below
-      if (rec) pw.template phaseB_entry<true>(bac, lacc, NLr, active, wbuf, bua, bub, bdiag);
-      else pw.template phaseB_entry<false>(bac, lacc, NLr, active, wbuf, bua, bub, bdiag);
+      const int warp = tid >> 5;
+      if (warp == W - 1) {
+        const int r = tid & 31;
+        if (r < 8) invert_P_group<I>(Pd, Pinv, rhsv, r, rec, ldet, a.status, group, active && crank == 0);
+      } else {
+        R* wbuf = (R*)wpart + warp * 32 * Shape<I, JM>::IWS;  // free until the reduction below
+        if (rec) pw.template phaseB_entry<true>(bac, lacc, NLr, active, wbuf, bua, bub, bdiag, warp, W - 1);
+        else pw.template phaseB_entry<false>(bac, lacc, NLr, active, wbuf, bua, bub, bdiag, warp, W - 1);
+      }
       FFCA_PROBE(3)
       if (rec) lacc = warp_sum_seg(lacc, 1);
       __syncthreads();  // every warp is done with its weight buffer (it aliases the partials)
@@ -1179,81 +1216,59 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
       __syncthreads();
       FFCA_PROBE(7)
     } else {
-      // I > 4: one group of 8 lanes per system (G == 1), row per lane (Gauss-Jordan).  Groups
-      // 0..I-1 invert B_i (Hermitian positive definite: no pivot search) while group mP -- the
-      // first group of the next warp, so the two paths never share a warp -- inverts P with
-      // partial pivoting; then group i applies B_i^-1 to [P^-H]_i.  B does not depend on P, so
-      // for K > 1 only the P inversion repeats.
+      // I > 4: thread i < I factors B_i = L D L^H in registers (Hermitian positive definite,
+      // fastfca.py:184-194 loading retry) and solves B_i x = [P^-H]_i with the P^-1 the last warp
+      // formed during phase B.  For K > 1 the later P^-1 come from the 8-lane group mP here.
       static_assert(G == 1, "I > 4 runs one bin per CTA");
       constexpr int mP = loop_pgroup(I);
-      const int m = tid >> 3, r = tid & 7;
-      const unsigned gmask = 0xFFu << (8 * ((tid >> 3) & 3));
-      double2* Binv = Msys;                         // I x I x I  (row-major per i)
-      double2* srow = Msys + I * I * I + m * 2 * I;  // group scratch
+      using LDL = PackedLDL<I>;
+      double2* Lsm = Msys + tid * LDL::NP;  // this thread's factor (the solver workspace is free)
+      if (tid < I) {
+        const double* T = tot + tid * I * I;
+        double tr = 0.0;
+#pragma unroll
+        for (int x = 0; x < I; ++x) tr += T[x * x];
+        tr *= invN;
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+          double2 b[LDL::NP];
+          int kk = 0;
+#pragma unroll
+          for (int x = 0; x < I; ++x) {
+#pragma unroll
+            for (int y2 = 0; y2 < x; ++y2) b[LDL::id(x, y2)] = make_double2(T[kk + 1 + 2 * y2] * invN, T[kk + 2 + 2 * y2] * invN);
+            b[LDL::id(x, x)] = make_double2(T[kk] * invN + (pass ? 1e-10 * tr : 0.0), 0.0);
+            kk += 1 + 2 * x;
+          }
+          const bool ok = LDL::factor(b);
+#pragma unroll
+          for (int e = 0; e < LDL::NP; ++e) Lsm[e] = b[e];
+          // one trace-loaded retry (fastfca.py:184-194)
+          if (pass == 1 && active && crank == 0) atomicOr(&a.status[group], ok ? ST_B_LOADED : ST_SINGULAR_B);
+          if (ok) break;
+        }
+      }
+      FFCA_PROBE(5)
 #pragma unroll 1
       for (int k = 0; k < a.K; ++k) {
-        if (m == mP) {
-          double2 ar[I], er[I];
-#pragma unroll
-          for (int c = 0; c < I; ++c) {
-            er[c] = make_double2(c == r ? 1.0 : 0.0, 0.0);
-            ar[c] = r < I ? Pd[r * I + c] : make_double2(0.0, 0.0);
-          }
-          int krow;
-          double ld = 0.0;
-          const bool ok = (rec && k == 0) ? gj_group<I, true>(ar, er, r, gmask, srow, krow, ld)
-                                          : gj_group<I, false>(ar, er, r, gmask, srow, krow, ld);
-          if (!ok && r == 0 && active && crank == 0) atomicOr(&a.status[group], ST_SINGULAR_P);
-          if (k == 0 && r == 0) ldet[0] = ld;
-          if (r < I)
-#pragma unroll
-            for (int c = 0; c < I; ++c) Pinv[krow * I + c] = er[c];
-        } else if (k == 0 && m < I) {
-          const double* T = tot + m * I * I;
-          double tr = 0.0;
-#pragma unroll
-          for (int x = 0; x < I; ++x) tr += T[x * x] * invN;
-#pragma unroll 1
-          for (int pass = 0; pass < 2; ++pass) {
-            double2 ar[I], er[I];
-#pragma unroll
-            for (int c = 0; c < I; ++c) {
-              er[c] = make_double2(c == r ? 1.0 : 0.0, 0.0);
-              if (r >= I) {
-                ar[c] = make_double2(0.0, 0.0);
-              } else {
-                const int hi = r >= c ? r : c, lo = r >= c ? c : r;
-                if (hi == lo) ar[c] = make_double2(T[hi * hi] * invN + (pass ? 1e-10 * tr : 0.0), 0.0);
-                else {
-                  const double re = T[hi * hi + 1 + 2 * lo] * invN, im = T[hi * hi + 2 + 2 * lo] * invN;
-                  ar[c] = make_double2(re, r >= c ? im : -im);
-                }
-              }
-            }
-            int krow;
-            double ld = 0.0;
-            const bool ok = gj_group<I, false, false>(ar, er, r, gmask, srow, krow, ld);
-            if (ok || pass == 1) {  // one trace-loaded retry (fastfca.py:184-194)
-              if (r < I)
-#pragma unroll
-                for (int c = 0; c < I; ++c) Binv[(m * I + krow) * I + c] = er[c];
-              if (pass == 1 && r == 0 && active && crank == 0) atomicOr(&a.status[group], ok ? ST_B_LOADED : ST_SINGULAR_B);
-              break;
-            }
-          }
+        if (k > 0) {
+          if ((tid >> 3) == mP) invert_P_group<I>(Pd, Pinv, rhsv, tid & 7, false, ldet, a.status, group, active && crank == 0);
+          __syncthreads();
         }
-        __syncthreads();
-        if (m < I && r < I) {
-          const int i = m;
-          double2 x = make_double2(0.0, 0.0);
+        if (tid < I) {
+          const int i = tid;
+          double2 z[I];
 #pragma unroll
-          for (int c = 0; c < I; ++c) {  // (B_i^-1)_{r,c} conj(P^-1_{i,c})
-            const double2 bq = Binv[(i * I + r) * I + c], pq = Pinv[i * I + c];
-            x.x += bq.x * pq.x + bq.y * pq.y;
-            x.y += bq.y * pq.x - bq.x * pq.y;
+          for (int x = 0; x < I; ++x) {  // [P^-H]_{x,i} = conj(P^-1_{i,x})
+            const double2 q = Pinv[i * I + x];
+            z[x] = make_double2(q.x, -q.y);
           }
-          Pd[r * I + i] = x;
-          Pc[r * I + i] = mk<C2, R>(R(x.x), R(x.y));
+          LDL::solve(Lsm, z);
+#pragma unroll
+          for (int x = 0; x < I; ++x) {
+            Pd[x * I + i] = z[x];
+            Pc[x * I + i] = mk<C2, R>(R(z[x].x), R(z[x].y));
+          }
         }
         __syncthreads();
       }
