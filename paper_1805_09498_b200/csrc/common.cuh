@@ -151,6 +151,7 @@ __device__ __forceinline__ double2 cmul(const double2 a, const double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 __device__ __forceinline__ double2 cadd(const double2 a, const double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(const double2 a, const double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ double2 crecip(const double2 z) {
   // 1/z = conj(z) / |z|^2; rescale by an exact power of two outside
   // [2^-500, 2^500] so |z|^2 neither overflows nor underflows.

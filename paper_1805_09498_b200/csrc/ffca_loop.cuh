@@ -256,8 +256,16 @@ __device__ __forceinline__ void bin_reduce(const R (&vals)[V], double* wpart, do
   bin_reduce_tail<G>(V, wpart, cpart, tot, C, VMAX, parity);
 }
 
+// 3 x 3 determinant of the rows r0 < r1 < r2 and columns c0 < c1 < c2 of a row-major 4 x 4 matrix.
+__device__ __forceinline__ double2 det3_of4(const double2* A, int r0, int r1, int r2, int c0, int c1, int c2) {
+  const double2 m0 = csub(cmul(A[r1 * 4 + c1], A[r2 * 4 + c2]), cmul(A[r1 * 4 + c2], A[r2 * 4 + c1]));
+  const double2 m1 = csub(cmul(A[r1 * 4 + c0], A[r2 * 4 + c2]), cmul(A[r1 * 4 + c2], A[r2 * 4 + c0]));
+  const double2 m2 = csub(cmul(A[r1 * 4 + c0], A[r2 * 4 + c1]), cmul(A[r1 * 4 + c1], A[r2 * 4 + c0]));
+  return cadd(csub(cmul(A[r0 * 4 + c0], m0), cmul(A[r0 * 4 + c1], m1)), cmul(A[r0 * 4 + c2], m2));
+}
+
 // Column c of the cofactor matrix of an I x I complex matrix A (row-major in shared memory,
-// I <= 3): out[x] = (-1)^(x+c) * minor(x, c), so that row c of A^-1 is out / det(A).  Elements are
+// I <= 4): out[x] = (-1)^(x+c) * minor(x, c), so that row c of A^-1 is out / det(A).  Elements are
 // read from shared memory as needed (no register copy of A).
 template <int I>
 __device__ __forceinline__ void adjugate_column(const double2* A, int c, double2 (&out)[I]) {
@@ -268,13 +276,22 @@ __device__ __forceinline__ void adjugate_column(const double2* A, int c, double2
     const double2 a1 = A[2 + (1 - c)], a0 = A[1 - c];
     out[0] = make_double2(sg * a1.x, sg * a1.y);
     out[1] = make_double2(-sg * a0.x, -sg * a0.y);
-  } else {
+  } else if constexpr (I == 3) {
     const int c1 = c == 0 ? 1 : 0, c2 = c == 2 ? 1 : 2;
 #pragma unroll
     for (int x = 0; x < 3; ++x) {
       const int r1 = x == 0 ? 1 : 0, r2 = x == 2 ? 1 : 2;
       const double2 p = cmul(A[r1 * 3 + c1], A[r2 * 3 + c2]), q = cmul(A[r1 * 3 + c2], A[r2 * 3 + c1]);
       const double2 m = make_double2(p.x - q.x, p.y - q.y);
+      out[x] = ((x + c) & 1) ? make_double2(-m.x, -m.y) : m;
+    }
+  } else {
+    static_assert(I == 4, "cofactors for I <= 4");
+    const int c0 = c == 0 ? 1 : 0, c1 = c <= 1 ? 2 : 1, c2 = c <= 2 ? 3 : 2;
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int r0 = x == 0 ? 1 : 0, r1 = x <= 1 ? 2 : 1, r2 = x <= 2 ? 3 : 2;
+      const double2 m = det3_of4(A, r0, r1, r2, c0, c1, c2);
       out[x] = ((x + c) & 1) ? make_double2(-m.x, -m.y) : m;
     }
   }
@@ -678,7 +695,7 @@ struct PointWork {
   // Frames past the bin's range get zero weights (their records are zero-filled or clamped).
   template <bool REC>
   __device__ __forceinline__ void phaseB_entry(C2 (&ac)[I], R& lacc, int NLr, bool active, R* wbuf, int ua, int ub,
-                                               bool diag, int warp, int W) const {
+                                               bool diag, int c0, int cstep) const {
     constexpr int IWS = Shape<I, JM>::IWS;
     const int lane = threadIdx.x & 31;
     R lam[JM][I];
@@ -690,7 +707,7 @@ struct PointWork {
     for (int i = 0; i < I; ++i) ac[i] = mk<C2, R>(R(0), R(0));
     const int nch = active ? (NLr + 31) / 32 : 0;
 #pragma unroll 1
-    for (int c = warp; c < nch; c += W) {
+    for (int c = c0; c < nch; c += cstep) {
       {  // reciprocal weights of frame 32c + lane
         const int n = 32 * c + lane;
         const bool ok = n < NLr;
@@ -703,12 +720,20 @@ struct PointWork {
 #pragma unroll
         for (int i = 0; i < IWS; ++i) iw[i] = R(0);
 #pragma unroll
-        for (int i = 0; i < I; ++i) {
+        for (int ip = 0; ip < I / 2; ++ip) {  // (w_2ip, w_2ip+1) pairs: FFMA2
+          C2 s2 = mk<C2, R>(R(0), R(0));
+#pragma unroll
+          for (int j = 0; j < JM; ++j)
+            if (j < J) s2 = fma2(bc2<R>(vj[j]), mk<C2, R>(lam[j][2 * ip], lam[j][2 * ip + 1]), s2);
+          iw[2 * ip] = ok ? rcp_pt(fmax(s2.x, wfl)) : R(0);
+          iw[2 * ip + 1] = ok ? rcp_pt(fmax(s2.y, wfl)) : R(0);
+        }
+        if constexpr (I & 1) {
           R s = R(0);
 #pragma unroll
           for (int j = 0; j < JM; ++j)
-            if (j < J) s = fma(vj[j], lam[j][i], s);
-          iw[i] = ok ? rcp_pt(fmax(s, wfl)) : R(0);
+            if (j < J) s = fma(vj[j], lam[j][I - 1], s);
+          iw[I - 1] = ok ? rcp_pt(fmax(s, wfl)) : R(0);
         }
         if constexpr (REC) {
           if (ok) {
@@ -731,13 +756,14 @@ struct PointWork {
 #pragma unroll 4
       for (int f = 0; f < nf; ++f, rec += RS) {
         const C2 ya = rec[ua], yb = rec[ub];
-        // complex unit: ya conj(yb) = yb.x (ya.x, ya.y) + yb.y (ya.y, -ya.x); diagonal pair: (|ya|^2, |yb|^2)
-        C2 z;
-        if (diag) {
-          z = mk<C2, R>(ya.x * ya.x + ya.y * ya.y, yb.x * yb.x + yb.y * yb.y);
-        } else {
-          z = fma2(mk<C2, R>(ya.y, -ya.x), bc2<R>(yb.y), fma2(ya, bc2<R>(yb.x), mk<C2, R>(R(0), R(0))));
-        }
+        // z = U V + X Z (two packed FMAs, the same for every lane; the FMA pipe is the bound):
+        // complex unit  ya conj(yb):  U = (ya.x, ya.y), V = (yb.x, yb.x), X = (ya.y, -ya.x), Z = (yb.y, yb.y)
+        // diagonal pair (|ya|^2, |yb|^2): U = V = (ya.x, yb.x), X = Z = (ya.y, yb.y)
+        const C2 U = mk<C2, R>(ya.x, diag ? yb.x : ya.y);
+        const C2 V = mk<C2, R>(diag ? ya.x : yb.x, yb.x);
+        const C2 X = mk<C2, R>(ya.y, diag ? yb.y : -ya.x);
+        const C2 Z = mk<C2, R>(diag ? ya.y : yb.y, yb.y);
+        const C2 z = fma2(U, V, fma2(X, Z, mk<C2, R>(R(0), R(0))));
         R wv[IWS];
         load_vec<IWS>(wbuf + f * IWS, wv);
 #pragma unroll
@@ -1045,8 +1071,11 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
         if (r < 8) invert_P_group<I>(Pd, Pinv, rhsv, r, rec, ldet, a.status, group, active && crank == 0);
       } else {
         R* wbuf = (R*)wpart + warp * 32 * Shape<I, JM>::IWS;  // free until the reduction below
-        if (rec) pw.template phaseB_entry<true>(bac, lacc, NLr, active, wbuf, bua, bub, bdiag, warp, W - 1);
-        else pw.template phaseB_entry<false>(bac, lacc, NLr, active, wbuf, bua, bub, bdiag, warp, W - 1);
+        // chunk c of the bin goes to warp c % (W - 1) (measured: giving the P warp's scheduler
+        // partner a double share made it the straggler)
+        const int c0 = warp, cstep = W - 1;
+        if (rec) pw.template phaseB_entry<true>(bac, lacc, NLr, active, wbuf, bua, bub, bdiag, c0, cstep);
+        else pw.template phaseB_entry<false>(bac, lacc, NLr, active, wbuf, bua, bub, bdiag, c0, cstep);
       }
       FFCA_PROBE(3)
       if (rec) lacc = warp_sum_seg(lacc, 1);
@@ -1090,10 +1119,8 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
     // ---------------- solve: P^-1 and new columns (fastfca.py:359-370) --------
     if constexpr (I <= 4) {
       // Thread (bin gg, s = 1 + i) factors B_i = L D L^H in registers, forms
-      // [P^-H]_i = conj(row i of P^-1) and solves B_i x = [P^-H]_i itself.  Row i of
-      // P^-1 comes from the adjugate for I <= 3 (each thread alone, no divergent
-      // branch); for I = 4 thread s == 0 factors P (LU, partial pivoting) and
-      // publishes the factors to the s >= 1 threads of its warp.
+      // [P^-H]_i = conj(row i of P^-1) from the adjugate (cofactors / det, each thread
+      // alone: no divergent LU thread, no publication step) and solves B_i x = [P^-H]_i.
       static_assert(G * (I + 1) <= 32, "the per-bin solver threads must be lanes of one warp");
       const int s = tid % (I + 1);
       const int gg = tid / (I + 1);
@@ -1129,12 +1156,11 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
       FFCA_PROBE(5)
 #pragma unroll 1
       for (int k = 0; k < a.K; ++k) {
-        if constexpr (I <= 3) {
-          // I <= 3: every solver thread forms its row of P^-1 from the adjugate (cofactors /
-          // det) -- no divergent LU thread and no publication step (measured: the LU thread
-          // and the LDL threads of one warp ran serially, 11 % of the iteration).  An exactly
-          // zero determinant flags SingularP, as an exactly zero LU pivot does for the
-          // structurally singular P the reference rejects (zero / repeated columns).
+        if constexpr (I <= 4) {
+          // Measured: a divergent LU thread and the LDL threads of one warp ran serially
+          // (11 % of the iteration at I = 3, 13 % at I = 4).  An exactly zero determinant flags
+          // SingularP, as an exactly zero LU pivot does for the structurally singular P the
+          // reference rejects (zero rows / columns).
           double2 z[I], det = make_double2(0.0, 0.0);
           if (bact && s > 0) {
             const double2* Pb = Pd + gg * I * I;
@@ -1165,53 +1191,7 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
             }
           }
           __syncwarp();
-          continue;
         }
-        if (bact && s == 0) {
-          SmallLU<I> lu;
-#pragma unroll
-          for (int x = 0; x < I; ++x)
-#pragma unroll
-            for (int y2 = 0; y2 < I; ++y2) lu.a[x][y2] = Pd[(gg * I + x) * I + y2];
-          if (rec && k == 0) lu.template factor<true>();
-          else lu.template factor<false>();
-          if (!lu.ok && crank == 0) atomicOr(&a.status[b], ST_SINGULAR_P);
-          if (rec && k == 0) ldet[gg] = lu.logabsdet;
-#pragma unroll
-          for (int x = 0; x < I; ++x) {
-#pragma unroll
-            for (int y2 = 0; y2 < I; ++y2) Ms[x * I + y2] = lu.a[x][y2];
-            Ms[I * I + x] = lu.rd[x];
-            pv[x] = lu.piv[x];
-          }
-        }
-        // all G*(I+1) <= 20 solver threads are lanes of warp 0: a warp barrier orders the
-        // LU publication (and, below, the column updates) -- the other warps go straight on
-        // to the block barrier after the loop
-        __syncwarp();
-        FFCA_PROBE(6)
-        if (bact && s > 0) {
-          const int i = s - 1;
-          SmallLU<I> lu;
-#pragma unroll
-          for (int x = 0; x < I; ++x) {
-#pragma unroll
-            for (int y2 = 0; y2 < I; ++y2) lu.a[x][y2] = Ms[x * I + y2];
-            lu.rd[x] = Ms[I * I + x];
-            lu.piv[x] = pv[x];
-          }
-          double2 z[I];
-          lu.inverse_row(i, z);
-#pragma unroll
-          for (int x = 0; x < I; ++x) z[x].y = -z[x].y;  // [P^-H]_{x,i} = conj(P^-1_{i,x})
-          ldl.solve(z);
-#pragma unroll
-          for (int x = 0; x < I; ++x) {
-            Pd[(gg * I + x) * I + i] = z[x];
-            Pc[(gg * I + x) * I + i] = mk<C2, R>(R(z[x].x), R(z[x].y));
-          }
-        }
-        __syncwarp();
       }
       __syncthreads();
       FFCA_PROBE(7)

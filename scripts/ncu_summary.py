@@ -78,3 +78,21 @@ ti = sum(v[1] for v in agg.values()) or 1
 print(f"\nper-source-line (top {top} by stall samples): file:line samples% inst% source")
 for k, v in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
     print(f"  {k[0]}:{k[1]}  {100 * v[0] / ts:5.1f}%  {100 * v[1] / ti:5.1f}%  {src[k].strip()[:90]}")
+
+# optional: SASS-level view -- the hottest instructions with their dominant stall reasons
+if len(sys.argv) > 3 and sys.argv[3] == "--sass":
+    nsass = int(sys.argv[4]) if len(sys.argv) > 4 else 40
+    rows = list(csv.reader(io.StringIO(ncu("--page", "source", "--csv", "--print-source", "sass"))))
+    h = rows[1]
+    body = [r for r in rows[2:] if len(r) == len(h)]
+    ix = {k: i for i, k in enumerate(h)}
+    reasons = [k for k in h if k.startswith("stall_") and "Not Issued" not in k]
+    tot = sum(float(r[ix["Warp Stall Sampling (All Samples)"]] or 0) for r in body) or 1
+    print(f"\nSASS (top {nsass} by stall samples): addr samples% execs reasons")
+    hot = sorted(range(len(body)), key=lambda i: -float(body[i][ix["Warp Stall Sampling (All Samples)"]] or 0))[:nsass]
+    for i in sorted(hot):
+        r = body[i]
+        smp = float(r[ix["Warp Stall Sampling (All Samples)"]] or 0)
+        rs = sorted(((float(r[ix[k]] or 0), k[6:]) for k in reasons), reverse=True)[:3]
+        print(f"  {i:6d} {100 * smp / tot:5.2f}% {r[ix['Instructions Executed']]:>9s}  {r[1].strip()[:60]:60s} "
+              + " ".join(f"{k}:{int(v)}" for v, k in rs if v > 0))
