@@ -183,6 +183,7 @@ static int launch_problem(int device, const DevProblem& d, cudaStream_t s) {
   a.status = d.status;
   a.scratch = scratch;
   a.slab_bytes = (long long)p.slab;
+  a.packed = nullptr;
   a.L = p.L;
   LoopFn fn = d.dtype == FFCA_C64 ? loop_kernel_f32(d.I, d.J, p.G, p.resident)
                                   : loop_kernel_f64(d.I, d.J, p.G, p.resident);
@@ -196,6 +197,41 @@ static int launch_problem(int device, const DevProblem& d, cudaStream_t s) {
     FFCA_CK(cudaEventCreate(&ev1));
     FFCA_CK(cudaEventRecord(ev0, s));
   }
+  // Resident slabs are filled from contiguous images (one bulk-copy stream per CTA) that a
+  // coalesced pack pass writes first: the bins-fastest reference layout otherwise costs one
+  // 4-16 byte request per element and frame (odd F rules out wider vector copies).
+  void* packed = nullptr;
+  // Measured: worth it for the one-CTA-per-SM I > 4 plans (config 4: gather 125k -> 6k cycles per
+  // CTA, 15.7 -> 15.2 ms), where nothing else on the SM hides the element gather; with two or more
+  // CTAs per SM the extra pass over HBM costs more than it saves (config 3: 16.8 -> 17.2 ms,
+  // config 2: 8.0 -> 8.2 ms).  FFCA_FORCE_PACK=1 enables it for every resident plan (tests).
+  const bool pack_plan = p.G == 1 && loop_interleaved(d.I);
+  if (p.resident && d.vf_mode != 2 && !getenv("FFCA_NO_PACK") && (pack_plan || getenv("FFCA_FORCE_PACK"))) {
+    FFCA_CK(cudaMallocAsync(&packed, size_t(p.grid) * p.slab, s));
+    PackArgs pa;
+    pa.y = d.y; pa.v = d.v0; pa.packed = packed;
+    pa.I = d.I; pa.J = d.J; pa.N = d.N; pa.F = d.F; pa.G = p.G; pa.C = p.C;
+    const int JM = hot_shape(d.I, d.J) ? d.J : 8;
+    pa.RS = loop_rs(d.I, JM);
+    pa.JS = loop_js(d.I, JM, d.J);
+    pa.ilv = loop_interleaved(d.I) ? 1 : 0;
+    pa.total_bins = nb;
+    pa.ngroups = (nb + p.G - 1) / p.G;
+    pa.slab_bytes = (long long)p.slab;
+    pa.Ly = (long long)p.L.y;
+    pa.Lv = (long long)p.L.v;
+    const size_t per_frame = 32 * (size_t(d.I) * 2 * rsize(d.dtype) + size_t(d.J) * rsize(d.dtype));
+    int FT = 32;
+    while (FT > 4 && FT * per_frame > 40 * 1024) FT >>= 1;
+    pa.FT = FT;
+    const size_t psm = FT * per_frame;
+    dim3 grid(unsigned((nb + 31) / 32), unsigned((d.N + FT - 1) / FT));
+    if (d.dtype == FFCA_C64) slab_pack_kernel<float><<<grid, 256, psm, s>>>(pa);
+    else slab_pack_kernel<double><<<grid, 256, psm, s>>>(pa);
+    FFCA_CK(cudaGetLastError());
+    count_launch();
+    a.packed = packed;
+  }
   FFCA_TRY(launch_loop(fn, p, a, s));
   FFCA_CK(cudaGetLastError());
   if (ev0) {
@@ -208,6 +244,7 @@ static int launch_problem(int device, const DevProblem& d, cudaStream_t s) {
     cudaEventDestroy(ev1);
   }
   if (scratch) FFCA_CK(cudaFreeAsync(scratch, s));
+  if (packed) FFCA_CK(cudaFreeAsync(packed, s));
   return FFCA_OK;
 }
 

@@ -34,6 +34,7 @@ namespace ffca {
 #define FFCA_PROBE_T1 1  // second probed thread (e.g. 64: the P group of the I > 4 solve)
 #endif
 __device__ unsigned long long g_phase[16];
+__device__ unsigned long long g_fixed[4];  // thread 0 of the middle CTA: gather, floor, write-back cycles
 #define FFCA_PROBE_INIT                                                       \
   long long _pt = clock64();                                                  \
   const bool _pr = (blockIdx.x == gridDim.x / 2) && (threadIdx.x == 0 || threadIdx.x == FFCA_PROBE_T1);
@@ -43,9 +44,14 @@ __device__ unsigned long long g_phase[16];
     atomicAdd(&g_phase[(k) + 8 * (threadIdx.x != 0)], (unsigned long long)(_n - _pt));           \
     _pt = _n;                                                                                    \
   }
+#define FFCA_FIXED_T0 const long long _ft0 = clock64();
+#define FFCA_FIXED(k)                                                                   \
+  if (blockIdx.x == gridDim.x / 2 && threadIdx.x == 0) g_fixed[k] += clock64() - _ft0;
 #else
 #define FFCA_PROBE_INIT
 #define FFCA_PROBE(k)
+#define FFCA_FIXED_T0
+#define FFCA_FIXED(k)
 #endif
 
 
@@ -166,6 +172,8 @@ struct LoopArgs {
   double* vf_out;      // optional (U, F): the floor actually used
   double* ll;          // optional (total_bins, 1 + 2*iters): per-bin likelihood parts
   int* status;         // (total_bins)
+  const void* packed;  // optional: slab images (slab_bytes per CTA, in blockIdx order) written by
+                       // slab_pack_kernel; resident CTAs then fill their slab with bulk copies
   void* scratch;       // non-resident slab storage (slab_bytes per CTA)
   long long slab_bytes;
   LoopSmem L;          // shared-memory carve-up, computed once on the host (kernel reads it from
@@ -813,6 +821,87 @@ __device__ __forceinline__ void invert_P_group(const double2* Pd, double2* Pinv,
     for (int c = 0; c < I; ++c) Pinv[krow * I + c] = er[c];
 }
 
+// Slab images for the bulk gather: a 256-thread CTA reads a tile of 32 consecutive bins x FT
+// frames of y (U, I, N, F) and v (U, J, N, F) with bin-contiguous (coalesced) loads into shared
+// memory, then writes each group's records in the loop kernel's slab order -- consecutive lanes
+// write consecutive record words of one image.  Records past a bin's channels / sources are zero
+// padding; bins past the end are zero.  Frames are mapped to the cluster rank that owns them.
+struct PackArgs {
+  const void* y;
+  const void* v;
+  void* packed;
+  int I, J, N, F, G, C, RS, JS, FT;
+  int ilv;
+  long long total_bins, ngroups, slab_bytes;
+  long long Ly, Lv;  // record regions inside an image
+};
+
+template <typename R>
+__global__ void __launch_bounds__(256) slab_pack_kernel(const PackArgs a) {
+  using C2 = typename Cpx<R>::T;
+  extern __shared__ __align__(16) unsigned char psm[];
+  __shared__ int rk[32], nlk[32];  // cluster rank / local frame of each tile frame
+  const int I = a.I, J = a.J, N = a.N, F = a.F, G = a.G, C = a.C, RS = a.RS, JS = a.JS, FT = a.FT;
+  C2* yt = (C2*)psm;               // [FT][32][I]
+  R* vt = (R*)(yt + FT * 32 * I);  // [FT][32][J]
+  const int tid = threadIdx.x;
+  const long long b0 = (long long)blockIdx.x * 32;
+  const int m0 = blockIdx.y * FT;
+  const int nf = min(FT, N - m0);
+  const C2* yg = (const C2*)a.y;
+  const R* vg = (const R*)a.v;
+  if (tid < FT) {
+    const int n = m0 + tid;
+    int r = int((long long)n * C / N);
+    while (r + 1 < C && (long long)(r + 1) * N / C <= n) ++r;
+    while (r > 0 && (long long)r * N / C > n) --r;
+    rk[tid] = r;
+    nlk[tid] = n - int((long long)r * N / C);
+  }
+  // this lane's bin (the same for every pass: 256 threads = 8 rows of 32 bins)
+  const int bl = tid & 31, row0 = tid >> 5;
+  const long long bin = b0 + bl;
+  const bool bok = bin < a.total_bins;
+  const long long u = bok ? bin / F : 0, f = bok ? bin % F : 0;
+  const C2* yb = yg + (u * I * (long long)N + m0) * F + f;
+  const R* vb = vg + (u * J * (long long)N + m0) * F + f;
+  for (int t = row0; t < I * FT; t += 8) {  // t = i * FT + nt
+    const int nt = t % FT, i = t / FT;
+    yt[(nt * 32 + bl) * I + i] = (bok && nt < nf) ? yb[((long long)i * N + nt) * F] : mk<C2, R>(R(0), R(0));
+  }
+  for (int t = row0; t < J * FT; t += 8) {
+    const int nt = t % FT, j = t / FT;
+    vt[(nt * 32 + bl) * J + j] = (bok && nt < nf) ? vb[((long long)j * N + nt) * F] : R(0);
+  }
+  __syncthreads();
+  // one record per thread and pass: (frame nt, group qi, bin g); records of one group and frame
+  // are adjacent in the image, so a warp writes a few contiguous runs
+  for (int t = tid; t < nf * 32; t += blockDim.x) {
+    const int nt = t >> 5, col = t & 31, qi = col / G, g = col % G;
+    const long long q = b0 / G + qi;
+    if (q >= a.ngroups) continue;
+    unsigned char* img = (unsigned char*)a.packed + (q * C + rk[nt]) * a.slab_bytes;
+    const int rec = nlk[nt] * G + g;
+    C2* yr = (C2*)(img + a.Ly) + (long long)rec * RS;
+    const C2* src = yt + (nt * 32 + col) * I;
+    const R* vsrc = vt + (nt * 32 + col) * J;
+    for (int s = 0; s < RS; ++s) {
+      C2 val = mk<C2, R>(R(0), R(0));
+      if (s < I) {
+        val = src[s];
+      } else if (a.ilv) {  // interleaved record: the J powers follow the I observations
+        const int j = 2 * (s - I);
+        val = mk<C2, R>(j < J ? vsrc[j] : R(0), j + 1 < J ? vsrc[j + 1] : R(0));
+      }
+      yr[s] = val;
+    }
+    if (!a.ilv) {
+      R* vr = (R*)(img + a.Lv) + (long long)rec * JS;
+      for (int j = 0; j < JS; ++j) vr[j] = j < J ? vsrc[j] : R(0);
+    }
+  }
+}
+
 template <typename R, int I, int JT, int G, bool RES>
 __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffca_loop_kernel(const LoopArgs a) {
   using C2 = typename Cpx<R>::T;
@@ -871,13 +960,27 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
 
   const C2* __restrict__ yg = (const C2*)a.y;
   const R* __restrict__ vg = (const R*)a.v_in;
+  FFCA_FIXED_T0
 
   // ---------------- load: gather (I,N,F) -> slab records ----------------
   // Consecutive lanes take consecutive bins g of the group, then frames, so a
   // warp reads whole 32-byte sectors of y[i, n, f..f+G).  Resident slabs are
   // filled with cp.async (zero-fill for padding), keeping every load of the
   // thread in flight at once.
-  {
+  __shared__ unsigned long long gather_bar;
+  if (a.packed && resident) {
+    // one TMA-engine bulk copy stream of this CTA's contiguous slab image (y and v records)
+    const unsigned bytes = unsigned(L.ybytes + L.vbytes);
+    if (tid == 0) {
+      mbar_init(&gather_bar, 1);
+      mbar_expect_tx(&gather_bar, bytes);
+      const unsigned char* src = (const unsigned char*)a.packed + (long long)blockIdx.x * a.slab_bytes;
+      constexpr unsigned CH = 32768;
+      for (unsigned o = 0; o < bytes; o += CH) bulk_g2s(smem + o, src + o, bytes - o < CH ? bytes - o : CH, &gather_bar);
+    }
+    __syncthreads();  // the barrier is initialised before anyone waits on it
+  }
+  if (!(a.packed && resident)) {
     const R* vfg = (const R*)a.vf;
     if (resident) {
 #pragma unroll 1
@@ -933,7 +1036,16 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
     lamc[t] = R(l);
   }
   cp_async_wait_all();
+  if (a.packed && resident) {
+    mbar_wait(&gather_bar, 0);
+    if (NL > NLr) {  // frames past this CTA's range: zero records, as the element gather leaves them
+      for (int t = tid; t < (NL - NLr) * G * RS; t += blockDim.x) ys[NLr * G * RS + t] = mk<C2, R>(R(0), R(0));
+      if (!Shape<I, JM>::ILV)
+        for (int t = tid; t < (NL - NLr) * G * JS; t += blockDim.x) vs[NLr * G * JS + t] = R(0);
+    }
+  }
   __syncthreads();
+  FFCA_FIXED(0)
 
   // ---------------- v floor per bin (fca.py:82-89 when auto) ----------------
   if (a.vf_mode == 3) {
@@ -1282,6 +1394,7 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
   }
 
   // ---------------- write back ----------------
+  FFCA_FIXED(1)
   R* vo = (R*)a.v_out;
   if (active)
     for (int j = 0; j < J; ++j)
@@ -1304,6 +1417,7 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
       }
     }
   }
+  FFCA_FIXED(2)
   // no CTA may exit while a peer can still read its shared memory
   if (C > 1) cg::this_cluster().sync();
 }

@@ -42,6 +42,12 @@ LoopFn loop_kernel_f32(int I, int J, int G, bool res) {
 }  // namespace ffca
 
 #ifdef FFCA_PHASE_PROBE
+extern "C" int ffca_debug_fixed(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, ffca::g_fixed, sizeof(unsigned long long) * 4);
+  unsigned long long z[4] = {};
+  cudaMemcpyToSymbol(ffca::g_fixed, z, sizeof(z));
+  return 0;
+}
 extern "C" int ffca_debug_phase(unsigned long long* out) {
   cudaMemcpyFromSymbol(out, ffca::g_phase, sizeof(unsigned long long) * 16);
   unsigned long long z[16] = {};

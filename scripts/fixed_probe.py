@@ -1,0 +1,31 @@
+"""Cycles of the loop kernel's one-time parts (gather, floor + loop, write-back) in the probe build
+(make EXTRA=-DFFCA_PHASE_PROBE BUILD=../../build/probe OUT=../../build/libffca_probe.so)."""
+import ctypes, os, sys
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+sys.path.insert(0, ROOT)
+import numpy as np
+import torch
+from paper_1805_09498_b200 import _lib
+_lib.LIB_PATH = os.path.join(ROOT, "build", "libffca_probe.so")
+from paper_1805_09498_b200.workloads import CONFIGS, make_torch
+
+cid = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+its = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+cfg = CONFIGS[cid]
+U = cfg.mixtures
+dev = torch.device("cuda", 0)
+lib = _lib.require_gpu()
+lib.ffca_debug_fixed.argtypes = [ctypes.c_void_p]
+y, P0, l0, v0 = make_torch(cfg, 7, U, dev)
+P, l, v = torch.empty_like(P0), torch.empty_like(l0), torch.empty_like(v0)
+code = _lib.C64 if cfg.dtype == "c64" else _lib.C128
+out = np.zeros(4, np.uint64)
+for rep in range(2):
+    lib.ffca_debug_fixed(out.ctypes.data)
+    _lib.check(lib.ffca_fastfca_run(0, None, _lib.MEM_DEVICE, code, U, cfg.I, cfg.J, cfg.N, cfg.F, y.data_ptr(),
+                                    P0.data_ptr(), l0.data_ptr(), v0.data_ptr(), _lib.VF_AUTO, 0.0, None,
+                                    its, 1, 0, P.data_ptr(), l.data_ptr(), v.data_ptr(), None, None, None))
+    torch.cuda.synchronize()
+lib.ffca_debug_fixed(out.ctypes.data)
+print(f"config {cid}, {its} iterations, middle CTA thread 0 cycles since kernel entry: gather {out[0]}, "
+      f"before write-back {out[1]}, after write-back {out[2]} (write-back {int(out[2]) - int(out[1])})")

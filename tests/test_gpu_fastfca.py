@@ -189,6 +189,31 @@ def test_forced_plans_agree(plan, dt):
     assert abs(run.loglik_after_p[-1] - base.loglik_after_p[-1]) <= lltol * abs(base.loglik_after_p[-1])
 
 
+@pytest.mark.parametrize("plan", [None, "1,2,1", "1,4,1", "4,1,1", "2,1,1", "1,1,1"])
+@pytest.mark.parametrize("dt", ["c128", "c64"])
+def test_packed_slab_gather_agrees(plan, dt):
+    # slab images written by the pack pass and bulk-copied into shared memory (the default for the
+    # I > 4 one-CTA-per-SM plans; forced here for every resident plan): bitwise the element gather,
+    # incl. uneven cluster frame splits (N = 150 over 4 ranks) and groups straddling mixtures
+    U, I, J, F, N = 3, 3, 3, 11, 150
+    ys, Ps, ls, vs = [], [], [], []
+    for u in range(U):
+        y, P0, lam0, v0, _ = mixture(80 + u, I, J, F, N, 4, 0.0)
+        y, P0, lam0, v0 = cast(dt, y, P0, lam0, v0)
+        ys.append(y); Ps.append(P0); ls.append(lam0); vs.append(v0)
+    y, P0, lam0, v0 = (np.stack(a) for a in (ys, Ps, ls, vs))
+    if plan:
+        os.environ["FFCA_FORCE_PLAN"] = plan
+    base = fastfca.run_fastfca_batch(y, P0, lam0, v0, iterations=4, record_likelihood=True)
+    os.environ["FFCA_FORCE_PACK"] = "1"
+    try:
+        run = fastfca.run_fastfca_batch(y, P0, lam0, v0, iterations=4, record_likelihood=True)
+    finally:
+        os.environ.pop("FFCA_FORCE_PACK", None)
+    for a, b in zip(run, base):
+        assert np.array_equal(a, b)
+
+
 def test_long_recording_slice_cluster_path():
     # config-2 shape (I=J=4, N=9375, rank-8 NMF, complex64) on a few bins: the
     # bin is longer than one CTA's shared memory, so a cluster splits the frames
