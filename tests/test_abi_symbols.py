@@ -58,8 +58,11 @@ def test_plan_introspection_without_device():
     # config 2 shape (c64, I=J=4, N=9375): a cluster splits the frames
     assert lib.ffca_plan_loop(0, _lib.C64, 1, 4, 4, 9375, 1025, _lib.VF_AUTO, out.ctypes.data_as(_lib._ip)) == 0
     assert out[1] > 1 and out[4] == 1
-    # config 4 shape (c64, I=8, J=6, N=4000): one CTA per bin, slab in global scratch
+    # config 4 shape (c64, I=8, J=6, N=4000): a CTA pair per bin, interleaved records resident
     assert lib.ffca_plan_loop(0, _lib.C64, 1, 8, 6, 4000, 2049, _lib.VF_AUTO, out.ctypes.data_as(_lib._ip)) == 0
+    assert out[1] == 2 and out[4] == 1 and out[3] == 256
+    # a longer 8-channel bin no longer fits a CTA quad: slab in L2-resident global scratch
+    assert lib.ffca_plan_loop(0, _lib.C64, 1, 8, 6, 12000, 2049, _lib.VF_AUTO, out.ctypes.data_as(_lib._ip)) == 0
     assert out[1] == 1 and out[4] == 0 and out[3] == 256
     # config 0 shape (c128): 2 bins per CTA
     assert lib.ffca_plan_loop(0, _lib.C128, 1, 3, 3, 626, 513, _lib.VF_AUTO, out.ctypes.data_as(_lib._ip)) == 0
