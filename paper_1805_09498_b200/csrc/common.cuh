@@ -266,104 +266,10 @@ __device__ double lu_logabsdet(const double2* a) {
 }
 
 // ------------------------------------------------------------------------
-// Register-resident small solvers (fully unrolled; static indexing only, so
-// the matrices stay in registers for I <= 4).  Used by the loop kernel's
-// per-bin P update:
-//   lu_p:   partial-pivoting LU of P (pivot |re|+|im|, LAPACK izamax), with the
-//           reciprocal pivots kept so the solves need no division.
-//   ldl_b:  LDL^H of the Hermitian weighted covariance B_i.
-// Both report an exactly zero pivot, which is when numpy.linalg.inv raises.
+// Register-resident LDL^H of the Hermitian weighted covariance B_i (fully
+// unrolled; static indexing only, so the factors stay in registers for
+// I <= 4).  Reports an exactly zero pivot, when numpy.linalg.inv raises.
 // ------------------------------------------------------------------------
-template <int I>
-struct SmallLU {
-  double2 a[I][I];  // L (unit, strictly lower) and U
-  double2 rd[I];    // 1 / U_kk
-  int piv[I];
-  bool ok;
-  double logabsdet;
-
-  template <bool LOGDET = true>
-  __device__ __forceinline__ void factor() {
-    ok = true;
-    logabsdet = 0.0;
-#pragma unroll
-    for (int k = 0; k < I; ++k) {
-      int p = k;
-      double best = cabs1(a[k][k]);
-#pragma unroll
-      for (int r = k + 1; r < I; ++r) {
-        const double m = cabs1(a[r][k]);
-        if (m > best) { best = m; p = r; }
-      }
-      piv[k] = p;
-#pragma unroll
-      for (int r = k + 1; r < I; ++r) {
-        const bool sw = (r == p);
-#pragma unroll
-        for (int c = 0; c < I; ++c) {
-          const double2 t = a[k][c];
-          a[k][c] = sw ? a[r][c] : t;
-          a[r][c] = sw ? t : a[r][c];
-        }
-      }
-      const double2 d = a[k][k];
-      if (d.x == 0.0 && d.y == 0.0) ok = false;
-      rd[k] = crecip(d);
-      if (LOGDET) logabsdet += log(hypot(d.x, d.y));
-#pragma unroll
-      for (int r = k + 1; r < I; ++r) {
-        const double2 l = cmul(a[r][k], rd[k]);
-        a[r][k] = l;
-#pragma unroll
-        for (int c = k + 1; c < I; ++c) {
-          const double2 u = a[k][c];
-          a[r][c].x -= l.x * u.x - l.y * u.y;
-          a[r][c].y -= l.x * u.y + l.y * u.x;
-        }
-      }
-    }
-  }
-
-  // z = row `row` of A^{-1}, i.e. the solution of A^T z = e_row.
-  // With S A = L U (S the row swaps): U^T w = e, L^T t = w, z = S^T t.
-  __device__ __forceinline__ void inverse_row(int row, double2 (&z)[I]) const {
-    double2 w[I];
-#pragma unroll
-    for (int r = 0; r < I; ++r) {
-      double2 acc = make_double2(r == row ? 1.0 : 0.0, 0.0);
-#pragma unroll
-      for (int c = 0; c < r; ++c) {  // (U^T)_{r,c} = U_{c,r}
-        const double2 u = a[c][r];
-        acc.x -= u.x * w[c].x - u.y * w[c].y;
-        acc.y -= u.x * w[c].y + u.y * w[c].x;
-      }
-      w[r] = cmul(acc, rd[r]);
-    }
-#pragma unroll
-    for (int r = I - 1; r >= 0; --r) {
-      double2 acc = w[r];
-#pragma unroll
-      for (int c = r + 1; c < I; ++c) {  // (L^T)_{r,c} = L_{c,r}
-        const double2 l = a[c][r];
-        acc.x -= l.x * z[c].x - l.y * z[c].y;
-        acc.y -= l.x * z[c].y + l.y * z[c].x;
-      }
-      z[r] = acc;
-    }
-    // undo the swaps in reverse order: z = S^T t
-#pragma unroll
-    for (int k = I - 1; k >= 0; --k) {
-#pragma unroll
-      for (int r = k + 1; r < I; ++r) {
-        const bool sw = (r == piv[k]);
-        const double2 t = z[k];
-        z[k] = sw ? z[r] : t;
-        z[r] = sw ? t : z[r];
-      }
-    }
-  }
-};
-
 template <int I>
 struct SmallLDL {
   double2 l[I][I];  // strictly lower part used
@@ -499,11 +405,9 @@ __device__ __forceinline__ double2 crecip_fast(const double2 z) {
   return crecip(z);
 }
 
-// PIVOT = false (Hermitian positive definite A, whose Schur complements stay HPD): row k is
-// the pivot of step k, no search; a pivot that is not > 0 in magnitude flags failure, like a
-// failed LDL^H.  The step loop stays rolled (instruction-cache footprint); column k of the
-// lane's row is picked with selects so a[] / e[] stay in registers.
-template <int I, bool LOGDET, bool PIVOT = true>
+// The step loop stays rolled (instruction-cache footprint); column k of the lane's row is picked
+// with selects so a[] / e[] stay in registers.
+template <int I, bool LOGDET>
 __device__ __forceinline__ bool gj_group(double2 (&a)[I], double2 (&e)[I], int r, unsigned gmask, double2* srow,
                                          int& k_of_row, double& logabsdet) {
   bool used = r >= I;
@@ -516,19 +420,16 @@ __device__ __forceinline__ bool gj_group(double2 (&a)[I], double2 (&e)[I], int r
 #pragma unroll
     for (int c = 1; c < I; ++c)
       if (c == k) ak = a[c];
-    int who = k;
-    if constexpr (PIVOT) {
-      // max of |re|+|im| over the unused rows, lowest lane on ties, as three group-wide integer
-      // reductions on the (non-negative) double's bit pattern: high word (+1, so an unused row
-      // with an exactly zero entry still beats the used rows' 0), then low word, then lane
-      const double best = cabs1(ak);
-      const unsigned hi = used ? 0u : unsigned(__double2hiint(best)) + 1u;
-      const unsigned lo = unsigned(__double2loint(best));
-      const unsigned mh = __reduce_max_sync(gmask, hi);
-      const unsigned ml = __reduce_max_sync(gmask, hi == mh ? lo : 0u);
-      who = int(__reduce_min_sync(gmask, (hi == mh && lo == ml) ? unsigned(r) : 8u));
-      if (mh <= 1u && ml == 0u) ok = false;  // exactly zero (or no) pivot
-    }
+    // max of |re|+|im| over the unused rows, lowest lane on ties, as three group-wide integer
+    // reductions on the (non-negative) double's bit pattern: high word (+1, so an unused row
+    // with an exactly zero entry still beats the used rows' 0), then low word, then lane
+    const double best = cabs1(ak);
+    const unsigned hi = used ? 0u : unsigned(__double2hiint(best)) + 1u;
+    const unsigned lo = unsigned(__double2loint(best));
+    const unsigned mh = __reduce_max_sync(gmask, hi);
+    const unsigned ml = __reduce_max_sync(gmask, hi == mh ? lo : 0u);
+    const int who = int(__reduce_min_sync(gmask, (hi == mh && lo == ml) ? unsigned(r) : 8u));
+    if (mh <= 1u && ml == 0u) ok = false;  // exactly zero (or no) pivot
     const bool piv = (who == r);
     if (piv) {
 #pragma unroll
@@ -541,9 +442,6 @@ __device__ __forceinline__ bool gj_group(double2 (&a)[I], double2 (&e)[I], int r
     // every lane reads the unscaled pivot row and forms the same reciprocal; the pivot lane
     // scales its row, the others subtract (a_k / pivot) times it -- one uniform update
     const double2 d = srow[k];
-    if constexpr (!PIVOT) {
-      if (!(cabs1(d) > 0.0)) ok = false;
-    }
     const double2 inv = crecip_fast(d);
     if (LOGDET && piv) logabsdet += log(hypot(d.x, d.y));
     const double2 f = cmul(ak, inv);

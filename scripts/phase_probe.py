@@ -25,7 +25,7 @@ for rep in range(2):
                                     cfg.iterations, 1, 0, P.data_ptr(), l.data_ptr(), v.data_ptr(), None, None, None))
     torch.cuda.synchronize()
 lib.ffca_debug_phase(out.ctypes.data)
-names = ["A points", "A reduce", "lambda'+bar", "B points", "B reduce+copy+bar", "pre-LU (LDL)", "LU+publish", "solve+bar"]
+names = ["A points", "A reduce", "lambda'+bar", "B points", "B reduce+bar", "B_i factor (LDL)", "P^-1 (K > 1)", "solve+bar"]
 for t in range(2):
     tot = out[8 * t: 8 * t + 8].astype(float)
     print(f"thread {t}: total {tot.sum() / cfg.iterations:.0f} cycles/iteration")
