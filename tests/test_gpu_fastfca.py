@@ -214,6 +214,32 @@ def test_packed_slab_gather_agrees(plan, dt):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("IJ", [(5, 2), (6, 3), (7, 4), (8, 6)])
+@pytest.mark.parametrize("K", [1, 2])
+@pytest.mark.parametrize("plan", [None, "1,2,1,256"])
+@pytest.mark.parametrize("dt", ["c128", "c64"])
+def test_many_channels_against_oracle(IJ, K, plan, dt):
+    # I > 4 kernels: odd I (a diagonal pair with a dummy half in the phase-B units), runtime J
+    # (I = 5..7) and the config-4 instantiation (8, 6); K = 2 exercises the in-solve P^-1 of the
+    # later inner iterations; "1,2,1,256" is the config-4 plan (CTA pair, 256 threads, the last
+    # warp inverting P during phase B).  Likelihood recording covers log|det P| from that warp.
+    I, J = IJ
+    y, P0, lam0, v0, _ = mixture(40 + I + J, I, J, 3, 160, 4, 0.05)
+    ref = ffr.run_fastfca(y, P0, lam0, v0, iterations=3, inner_iterations=K, record_likelihood=True, stats=False)
+    y, P0, lam0, v0 = cast(dt, y, P0, lam0, v0)
+    if plan:
+        os.environ["FFCA_FORCE_PLAN"] = plan
+    run = fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=3,
+                              inner_iterations=K, record_likelihood=True)
+    tol = 1e-10 if dt == "c128" else 1e-4
+    assert rel(run.params.P, ref.P) <= tol
+    assert rel(run.params.Lam, ref.lam) <= tol
+    assert rel(run.params.v, ref.v) <= tol
+    ll = np.array([run.loglik_init] + run.loglik_after_em + run.loglik_after_p)
+    rll = np.array([ref.loglik_init] + ref.loglik_after_em + ref.loglik_after_p)
+    assert np.abs(ll - rll).max() <= (1e-10 if dt == "c128" else 1e-5) * np.abs(rll).max()
+
+
 def test_long_recording_slice_cluster_path():
     # config-2 shape (I=J=4, N=9375, rank-8 NMF, complex64) on a few bins: the
     # bin is longer than one CTA's shared memory, so a cluster splits the frames
