@@ -25,7 +25,14 @@ LoopFn loop_kernel_f32(int I, int J, int G, bool res) {
   if (I == 8 && J == 6) return hot<8, 6>(G, res);
   if (I == 2 && J == 2) return hot<2, 2>(G, res);
   if (J > 8 || G != 1) return nullptr;
-  // runtime J (<= 8); residency decided at run time (scratch == nullptr)
+  // runtime J (<= 8); residency decided at run time (scratch == nullptr) -- except the resident
+  // I > 4 plans, which run one CTA per SM and get the 255-register instantiation
+  if (res && I > 4) switch (I) {
+      case 5: return ffca_loop_kernel<float, 5, 0, 1, true>;
+      case 6: return ffca_loop_kernel<float, 6, 0, 1, true>;
+      case 7: return ffca_loop_kernel<float, 7, 0, 1, true>;
+      case 8: return ffca_loop_kernel<float, 8, 0, 1, true>;
+    }
   switch (I) {
     case 1: return ffca_loop_kernel<float, 1, 0, 1, false>;
     case 2: return ffca_loop_kernel<float, 2, 0, 1, false>;
