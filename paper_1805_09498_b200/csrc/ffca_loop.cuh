@@ -135,7 +135,7 @@ struct LoopSmem {
     bst = o;   // unused (the solves read the reduced sums in tot)
     {  // solver workspace: per-system matrices (I <= 4) or B_i^-1 + group rows (I > 4)
       const size_t m1 = size_t(G) * (I + 1) * I * I * 16, m2 = (size_t(I) * I * I + 2 * I * (loop_pgroup(I) + 1)) * 16;
-      size_t wp = align16(size_t(W) * G * VMAX * 8);
+      size_t wp = align16(size_t(W) * G * VMAX * rsz);  // warp partials in the compute type
       const size_t ms = align16(m1 > m2 ? m1 : m2);
       if (ilv) {  // I > 4 phase B: per-warp buffers of 32 frames' reciprocal weights
         const size_t wb = size_t(W) * 32 * ((I + 3) & ~3) * rsz;
@@ -197,8 +197,8 @@ __device__ __forceinline__ T bin_warp_sum(T x) {
 // Block / cluster half of the reduction: wpart[(warp*G + g)*VMAX + k] holds each
 // warp's partial for k < nv; sums over warps in index order, then cluster
 // ranks in rank order, into tot[g*VMAX + k].
-template <int G>
-__device__ __forceinline__ void bin_reduce_tail(int nv, double* wpart, double* cpart, double* tot, int C, int VMAX,
+template <int G, typename T>
+__device__ __forceinline__ void bin_reduce_tail(int nv, const T* wpart, double* cpart, double* tot, int C, int VMAX,
                                                 int& parity) {
   const int tid = threadIdx.x, W = blockDim.x >> 5;
   __syncthreads();
@@ -207,7 +207,7 @@ __device__ __forceinline__ void bin_reduce_tail(int nv, double* wpart, double* c
   for (int t = tid; t < G * nv; t += blockDim.x) {
     const int gg = t / nv, k = t % nv;
     double s = 0.0;
-    for (int w = 0; w < W; ++w) s += wpart[(w * G + gg) * VMAX + k];
+    for (int w = 0; w < W; ++w) s += double(wpart[(w * G + gg) * VMAX + k]);
     dst[gg * VMAX + k] = s;
   }
   if (C > 1) {
@@ -245,8 +245,8 @@ __device__ __forceinline__ void halving_step(R (&buf)[N], int lane, int& base) {
 // values and receives the partner's copy of that half, so the V values take
 // ~V shuffles instead of V*log2(L).  Lane with in-bin bits (b16..bG) ends up
 // owning values [base, base + V2/L), base = sum_s b_s * V2 / 2^(s+1).
-template <typename R, int V, int G>
-__device__ __forceinline__ void bin_reduce(const R (&vals)[V], double* wpart, double* cpart, double* tot, int C,
+template <typename R, int V, int G, typename T>
+__device__ __forceinline__ void bin_reduce(const R (&vals)[V], T* wpart, double* cpart, double* tot, int C,
                                            int VMAX, int& parity) {
   constexpr int L = 32 / G;
   constexpr int V2 = (V + L - 1) / L * L;
@@ -257,10 +257,10 @@ __device__ __forceinline__ void bin_reduce(const R (&vals)[V], double* wpart, do
   for (int k = 0; k < V2; ++k) buf[k] = k < V ? vals[k] : R(0);
   int base = 0;
   halving_step<R, V2, 16, G>(buf, lane, base);
-  double* row = wpart + (warp * G + g) * VMAX;
+  T* row = wpart + (warp * G + g) * VMAX;  // warp partials (the loop kernel keeps them in its compute type)
 #pragma unroll
   for (int k = 0; k < V2 / L; ++k)
-    if (base + k < V) row[base + k] = double(buf[k]);
+    if (base + k < V) row[base + k] = T(buf[k]);
   bin_reduce_tail<G>(V, wpart, cpart, tot, C, VMAX, parity);
 }
 
@@ -946,7 +946,7 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
   double* lamd = (double*)(smem + L.lamd);
   double* vfl = (double*)(smem + L.vfl);
   double* ldet = (double*)(smem + L.ldet);
-  double* wpart = (double*)(smem + L.wpart);
+  R* wpart = (R*)(smem + L.wpart);
   double* cpart = (double*)(smem + L.cpart);
   double* tot = (double*)(smem + L.tot);
   double2* Msys = (double2*)(smem + L.M);
@@ -1182,7 +1182,7 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
         const int r = tid & 31;
         if (r < 8) invert_P_group<I>(Pd, Pinv, rhsv, r, rec, ldet, a.status, group, active && crank == 0);
       } else {
-        R* wbuf = (R*)wpart + warp * 32 * Shape<I, JM>::IWS;  // free until the reduction below
+        R* wbuf = wpart + warp * 32 * Shape<I, JM>::IWS;  // free until the reduction below
         // chunk c of the bin goes to warp c % (W - 1) (measured: giving the P warp's scheduler
         // partner a double share made it the straggler)
         const int c0 = warp, cstep = W - 1;
@@ -1193,22 +1193,22 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
       if (rec) lacc = warp_sum_seg(lacc, 1);
       __syncthreads();  // every warp is done with its weight buffer (it aliases the partials)
       {
-        double* wp = wpart + (tid >> 5) * VMAX;
+        R* wp = wpart + (tid >> 5) * VMAX;
         if (bdiag) {
 #pragma unroll
           for (int i = 0; i < I; ++i) {
-            wp[i * I * I + bua * bua] = double(bac[i].x);
-            if (bub != bua) wp[i * I * I + bub * bub] = double(bac[i].y);
+            wp[i * I * I + bua * bua] = bac[i].x;
+            if (bub != bua) wp[i * I * I + bub * bub] = bac[i].y;
           }
         } else if (bown) {
           const int e = bua * bua + 1 + 2 * bub;
 #pragma unroll
           for (int i = 0; i < I; ++i) {
-            wp[i * I * I + e] = double(bac[i].x);
-            wp[i * I * I + e + 1] = double(bac[i].y);
+            wp[i * I * I + e] = bac[i].x;
+            wp[i * I * I + e + 1] = bac[i].y;
           }
         }
-        if ((tid & 31) == 0) wp[I * I * I] = double(lacc);
+        if ((tid & 31) == 0) wp[I * I * I] = lacc;
       }
       bin_reduce_tail<G>(I * I * I + 1, wpart, cpart, tot, C, VMAX, parity);
       if (rec && tid < G) llB = tot[tid * VMAX + I * I * I];
