@@ -20,9 +20,11 @@ code = _lib.C64 if cfg.dtype == "c64" else _lib.C128
 out = np.zeros(16, np.uint64)
 for rep in range(2):
     lib.ffca_debug_phase(out.ctypes.data)
-    _lib.check(lib.ffca_fastfca_run(0, None, _lib.MEM_DEVICE, code, U, cfg.I, cfg.J, cfg.N, cfg.F, y.data_ptr(),
+    rc = (lib.ffca_fastfca_run(0, None, _lib.MEM_DEVICE, code, U, cfg.I, cfg.J, cfg.N, cfg.F, y.data_ptr(),
                                     P0.data_ptr(), l0.data_ptr(), v0.data_ptr(), _lib.VF_AUTO, 0.0, None,
                                     cfg.iterations, 1, 0, P.data_ptr(), l.data_ptr(), v.data_ptr(), None, None, None))
+    if rc != 0:  # timing experiments (e.g. -DFFCA_SKIP_BLOOP) may produce singular results
+        print("note: call returned", rc, _lib.last_error())
     torch.cuda.synchronize()
 lib.ffca_debug_phase(out.ctypes.data)
 names = ["A points", "A reduce", "lambda'+bar", "B points", "B reduce+bar", "B_i factor (LDL)", "P^-1 (K > 1)", "solve+bar"]
