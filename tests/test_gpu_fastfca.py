@@ -240,6 +240,26 @@ def test_many_channels_against_oracle(IJ, K, plan, dt):
     assert np.abs(ll - rll).max() <= (1e-10 if dt == "c128" else 1e-5) * np.abs(rll).max()
 
 
+@pytest.mark.parametrize("plan", [None, "1,2,1,256", "1,4,1,256"])
+@pytest.mark.parametrize("dt", ["c128", "c64"])
+def test_many_channels_full_floor_array(plan, dt):
+    # I > 4 with a full (J, N, F) floor (vf_mode 2: the floor records ride in the slab, no pack
+    # pass), incl. CTA pairs / quads
+    I, J = 8, 6
+    y, P0, lam0, v0, _ = mixture(71, I, J, 3, 160, 4, 0.05)
+    vf = np.random.default_rng(5).uniform(0.0, 0.05, (J, 160, 3)) * v0.mean()
+    ref = ffr.run_fastfca(y, P0, lam0, v0, iterations=3, v_floor=vf, stats=False)
+    y, P0, lam0, v0 = cast(dt, y, P0, lam0, v0)
+    if plan:
+        os.environ["FFCA_FORCE_PLAN"] = plan
+    run = fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=3,
+                              v_floor=vf)
+    tol = 1e-10 if dt == "c128" else 1e-4
+    assert rel(run.params.P, ref.P) <= tol
+    assert rel(run.params.Lam, ref.lam) <= tol
+    assert rel(run.params.v, ref.v) <= tol
+
+
 def test_long_recording_slice_cluster_path():
     # config-2 shape (I=J=4, N=9375, rank-8 NMF, complex64) on a few bins: the
     # bin is longer than one CTA's shared memory, so a cluster splits the frames
