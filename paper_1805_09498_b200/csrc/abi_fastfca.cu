@@ -50,7 +50,7 @@ static int choose_threads(int G, int NL, int I) {
 }
 
 static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int vf_mode, LoopPlan& p,
-                     size_t smem_optin) {
+                     size_t smem_optin, int nsm = 148) {
   const int rsz = int(rsize(dtype));
   const int JM = hot_shape(I, J) ? J : 8;
   const int VMAX = host_vmax(I, JM);
@@ -84,6 +84,20 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
       }
       if (p.smem <= smem_optin) return FFCA_OK;
     }
+  }
+  // complex128, less than one wave of 2-bin CTAs (two per SM): one bin per 128-thread CTA
+  // spreads the bins over more SMs (four such CTAs fit an SM).  Measured: config 0 (513 bins)
+  // kernel 0.203 -> 0.197 ms; for complex64 the 4-bin CTAs stay faster (one config-3 mixture
+  // 0.109 vs 0.113 ms, two 0.161 vs 0.195 ms), so complex64 keeps G0.
+  if (dtype == FFCA_C128 && G0 > 1 && I <= 4 && (total_bins + G0 - 1) / G0 < 2LL * nsm) {
+    fill(1, 1, true);
+    if (p.threads > 128) {
+      p.threads = 128;
+      LoopSmem L(I, J, JM, 1, p.NL, 4, rsz, vf_mode, true, VMAX);
+      p.L = L;
+      p.smem = L.total;
+    }
+    if (p.slab <= kSlabBudget && p.smem <= smem_optin) return FFCA_OK;
   }
   for (int G : {G0, 1}) {
     fill(G, 1, true);
@@ -166,8 +180,10 @@ static int launch_problem(int device, const DevProblem& d, cudaStream_t s) {
   if (nb == 0) return FFCA_OK;
   int optin = 0;
   FFCA_CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  int nsm = 148;
+  FFCA_CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
   LoopPlan p;
-  FFCA_TRY(plan_loop(d.dtype, d.I, d.J, d.N, nb, d.vf_mode, p, size_t(optin)));
+  FFCA_TRY(plan_loop(d.dtype, d.I, d.J, d.N, nb, d.vf_mode, p, size_t(optin), nsm));
   void* scratch = nullptr;
   if (!p.resident) FFCA_CK(cudaMallocAsync(&scratch, size_t(p.grid) * p.slab, s));
   LoopArgs a;
