@@ -261,7 +261,7 @@ def run_ours(args, rank, world, local_rank):
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4),
                 "traffic": (tr or {}).get("dram_bytes_per_launch"),
-                "kernel": "ffca_loop_kernel<float,3,3,4,true>",
+                "kernel": "ffca_loop_kernel<float,3,3,2,true>",
                 "kernel_ms": round(k_ms, 4),
                 "algorithmic_bytes_per_unit": algo_bytes_pt,
                 "units_per_launch": units_launch,

@@ -52,9 +52,12 @@ def test_plan_introspection_without_device():
     from paper_1805_09498_b200 import _lib
     lib = _lib.load()
     out = np.zeros(6, np.int32)
-    # config 3 shape (c64, I=J=3, N=626): 4 lane-interleaved bins per CTA, resident
+    # config 3 shape (c64, I=J=3, N=626): 2 lane-interleaved bins per 128-thread CTA, resident
     assert lib.ffca_plan_loop(0, _lib.C64, 256, 3, 3, 626, 513, _lib.VF_AUTO, out.ctypes.data_as(_lib._ip)) == 0
-    assert out[0] == 4 and out[1] == 1 and out[4] == 1
+    assert out[0] == 2 and out[1] == 1 and out[3] == 128 and out[4] == 1
+    # other complex64 hot shapes keep 4 lane-interleaved bins
+    assert lib.ffca_plan_loop(0, _lib.C64, 64, 2, 2, 626, 513, _lib.VF_AUTO, out.ctypes.data_as(_lib._ip)) == 0
+    assert out[0] == 4
     # config 2 shape (c64, I=J=4, N=9375): a cluster splits the frames
     assert lib.ffca_plan_loop(0, _lib.C64, 1, 4, 4, 9375, 1025, _lib.VF_AUTO, out.ctypes.data_as(_lib._ip)) == 0
     assert out[1] > 1 and out[4] == 1
