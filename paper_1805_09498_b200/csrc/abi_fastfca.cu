@@ -350,24 +350,38 @@ static int pipelined_host_run(int device, cudaStream_t user, const DevProblem& p
   void *dy[2], *dP0[2], *dl0[2], *dv0[2], *dvf[2] = {nullptr, nullptr}, *dP[2], *dl[2], *dv[2], *dvo[2] = {nullptr, nullptr},
        *dst[2], *dll[2] = {nullptr, nullptr};
   int rc = FFCA_OK;
-  for (int k = 0; k < 2 && rc == FFCA_OK; ++k) {
-    rc = dalloc(bytes(By), &dy[k]);
-    if (!rc) rc = dalloc(bytes(BP), &dP0[k]);
-    if (!rc) rc = dalloc(bytes(Bl), &dl0[k]);
-    if (!rc) rc = dalloc(bytes(Bv), &dv0[k]);
-    if (!rc && proto.vf_mode == 1) rc = dalloc(bytes(Bvb), &dvf[k]);
-    if (!rc && proto.vf_mode == 2) rc = dalloc(bytes(Bv), &dvf[k]);
-    if (!rc) rc = dalloc(bytes(BP), &dP[k]);
-    if (!rc) rc = dalloc(bytes(Bl), &dl[k]);
-    if (!rc) rc = dalloc(bytes(Bv), &dv[k]);
-    if (!rc && vf_out) rc = dalloc(bytes(Bvo), &dvo[k]);
-    if (!rc) rc = dalloc(bytes(Bst), &dst[k]);
-    if (!rc && rec) rc = dalloc(bytes(Bll), &dll[k]);
-  }
   void *fstatus = nullptr, *fll = nullptr, *llmix = nullptr;
   if (!rc) rc = dalloc(size_t(nb) * 4, &fstatus);
   if (!rc && rec) rc = dalloc(size_t(nb) * nev * 8, &fll);
   if (!rc && rec && ll_out) rc = dalloc(size_t(U) * nev * 8, &llmix);
+  // Mixture chunks: the small per-bin arrays (P, lambda in and out, status, likelihood parts)
+  // are whole-batch device buffers moved with one copy each; only y / v (in) and v (out) move per
+  // chunk (each copy costs ~0.15 ms of fixed DMA / API overhead at ~23 chunks per call).
+  void *fP0 = nullptr, *fl0 = nullptr, *fP = nullptr, *fl = nullptr;
+  const size_t nP = size_t(nb) * I * I * cs, nl = size_t(U) * J * F * I * rs;
+  if (by_mixture && !rc) {
+    rc = dalloc(nP, &fP0);
+    if (!rc) rc = dalloc(nl, &fl0);
+    if (!rc) rc = dalloc(nP, &fP);
+    if (!rc) rc = dalloc(nl, &fl);
+    if (!rc) FFCA_CK(cudaMemcpyAsync(fP0, P0, nP, cudaMemcpyHostToDevice, sin));
+    if (!rc) FFCA_CK(cudaMemcpyAsync(fl0, lam0, nl, cudaMemcpyHostToDevice, sin));
+    if (!rc) FFCA_CK(cudaMemsetAsync(fstatus, 0, size_t(nb) * 4, sin));
+  }
+  for (int k = 0; k < 2 && rc == FFCA_OK; ++k) {
+    rc = dalloc(bytes(By), &dy[k]);
+    if (!rc && !by_mixture) rc = dalloc(bytes(BP), &dP0[k]);
+    if (!rc && !by_mixture) rc = dalloc(bytes(Bl), &dl0[k]);
+    if (!rc) rc = dalloc(bytes(Bv), &dv0[k]);
+    if (!rc && proto.vf_mode == 1) rc = dalloc(bytes(Bvb), &dvf[k]);
+    if (!rc && proto.vf_mode == 2) rc = dalloc(bytes(Bv), &dvf[k]);
+    if (!rc && !by_mixture) rc = dalloc(bytes(BP), &dP[k]);
+    if (!rc && !by_mixture) rc = dalloc(bytes(Bl), &dl[k]);
+    if (!rc) rc = dalloc(bytes(Bv), &dv[k]);
+    if (!rc && vf_out) rc = dalloc(bytes(Bvo), &dvo[k]);
+    if (!rc && !by_mixture) rc = dalloc(bytes(Bst), &dst[k]);
+    if (!rc && rec && !by_mixture) rc = dalloc(bytes(Bll), &dll[k]);
+  }
   int nch = 0;
   for (int c0 = 0; !rc && c0 < (by_mixture ? U : F); c0 += (by_mixture ? cu : cf), ++nch) {
     const int k = nch & 1;
@@ -379,38 +393,58 @@ static int pipelined_host_run(int device, cudaStream_t user, const DevProblem& p
       if (!rc) rc = cudaStreamWaitEvent(scomp, ev_out[k], 0) == cudaSuccess ? FFCA_OK : FFCA_E_CUDA;
     }
     if (!rc) rc = copy_blk(dy[k], y, By, U, F, u0, Uc, f0, Fc, true, sin);
-    if (!rc) rc = copy_blk(dP0[k], P0, BP, U, F, u0, Uc, f0, Fc, true, sin);
-    if (!rc) rc = copy_blk(dl0[k], lam0, Bl, U, F, u0, Uc, f0, Fc, true, sin);
+    if (!rc && !by_mixture) rc = copy_blk(dP0[k], P0, BP, U, F, u0, Uc, f0, Fc, true, sin);
+    if (!rc && !by_mixture) rc = copy_blk(dl0[k], lam0, Bl, U, F, u0, Uc, f0, Fc, true, sin);
     if (!rc) rc = copy_blk(dv0[k], v0, Bv, U, F, u0, Uc, f0, Fc, true, sin);
     if (!rc && proto.vf_mode == 1) rc = copy_blk(dvf[k], vf, Bvb, U, F, u0, Uc, f0, Fc, true, sin);
     if (!rc && proto.vf_mode == 2) rc = copy_blk(dvf[k], vf, Bv, U, F, u0, Uc, f0, Fc, true, sin);
     if (rc) break;
     FFCA_CK(cudaEventRecord(ev_in[k], sin));
     FFCA_CK(cudaStreamWaitEvent(scomp, ev_in[k], 0));
-    FFCA_CK(cudaMemsetAsync(dst[k], 0, size_t(Uc) * Fc * 4, scomp));
     DevProblem d = proto;
     d.U = Uc;
     d.F = Fc;
-    d.y = dy[k]; d.P0 = dP0[k]; d.lam0 = dl0[k]; d.v0 = dv0[k]; d.vf = dvf[k];
-    d.P = dP[k]; d.lam = dl[k]; d.v = dv[k]; d.vf_out = (double*)dvo[k];
-    d.ll_bins = (double*)dll[k];
-    d.status = (int*)dst[k];
+    d.y = dy[k]; d.v0 = dv0[k]; d.vf = dvf[k];
+    d.v = dv[k]; d.vf_out = (double*)dvo[k];
+    if (by_mixture) {  // views into the whole-batch buffers (mixture blocks are contiguous)
+      const size_t b0 = size_t(u0) * F;
+      d.P0 = (const char*)fP0 + b0 * I * I * cs;
+      d.lam0 = (const char*)fl0 + size_t(u0) * J * F * I * rs;
+      d.P = (char*)fP + b0 * I * I * cs;
+      d.lam = (char*)fl + size_t(u0) * J * F * I * rs;
+      d.status = (int*)fstatus + b0;
+      d.ll_bins = rec ? (double*)fll + b0 * nev : nullptr;
+    } else {
+      FFCA_CK(cudaMemsetAsync(dst[k], 0, size_t(Uc) * Fc * 4, scomp));
+      d.P0 = dP0[k]; d.lam0 = dl0[k];
+      d.P = dP[k]; d.lam = dl[k];
+      d.ll_bins = (double*)dll[k];
+      d.status = (int*)dst[k];
+    }
     rc = launch_problem(device, d, scomp);
     if (rc) break;
-    // scatter the per-bin status / likelihood parts into the full-size buffers
-    FFCA_CK(cudaMemcpy2DAsync((char*)fstatus + (size_t(u0) * F + f0) * 4, size_t(F) * 4, dst[k], size_t(Fc) * 4,
-                              size_t(Fc) * 4, size_t(Uc), cudaMemcpyDeviceToDevice, scomp));
-    if (rec)
-      FFCA_CK(cudaMemcpy2DAsync((char*)fll + (size_t(u0) * F + f0) * nev * 8, size_t(F) * nev * 8, dll[k],
-                                size_t(Fc) * nev * 8, size_t(Fc) * nev * 8, size_t(Uc), cudaMemcpyDeviceToDevice,
-                                scomp));
+    if (!by_mixture) {
+      // scatter the per-bin status / likelihood parts into the full-size buffers
+      FFCA_CK(cudaMemcpy2DAsync((char*)fstatus + (size_t(u0) * F + f0) * 4, size_t(F) * 4, dst[k], size_t(Fc) * 4,
+                                size_t(Fc) * 4, size_t(Uc), cudaMemcpyDeviceToDevice, scomp));
+      if (rec)
+        FFCA_CK(cudaMemcpy2DAsync((char*)fll + (size_t(u0) * F + f0) * nev * 8, size_t(F) * nev * 8, dll[k],
+                                  size_t(Fc) * nev * 8, size_t(Fc) * nev * 8, size_t(Uc), cudaMemcpyDeviceToDevice,
+                                  scomp));
+    }
     FFCA_CK(cudaEventRecord(ev_k[k], scomp));
     FFCA_CK(cudaStreamWaitEvent(sout, ev_k[k], 0));
-    rc = copy_blk(P_out, dP[k], BP, U, F, u0, Uc, f0, Fc, false, sout);
-    if (!rc) rc = copy_blk(lam_out, dl[k], Bl, U, F, u0, Uc, f0, Fc, false, sout);
+    if (!by_mixture) {
+      rc = copy_blk(P_out, dP[k], BP, U, F, u0, Uc, f0, Fc, false, sout);
+      if (!rc) rc = copy_blk(lam_out, dl[k], Bl, U, F, u0, Uc, f0, Fc, false, sout);
+    }
     if (!rc) rc = copy_blk(v_out, dv[k], Bv, U, F, u0, Uc, f0, Fc, false, sout);
     if (!rc && vf_out) rc = copy_blk(vf_out, dvo[k], Bvo, U, F, u0, Uc, f0, Fc, false, sout);
     if (!rc) FFCA_CK(cudaEventRecord(ev_out[k], sout));
+  }
+  if (!rc && by_mixture) {  // the whole-batch P / lambda after the last kernel
+    FFCA_CK(cudaMemcpyAsync(P_out, fP, nP, cudaMemcpyDeviceToHost, scomp));
+    FFCA_CK(cudaMemcpyAsync(lam_out, fl, nl, cudaMemcpyDeviceToHost, scomp));
   }
   if (!rc) {
     FFCA_CK(cudaStreamSynchronize(scomp));
