@@ -86,6 +86,20 @@ int ffca_fastfca_run(int device, void* stream, int mem, int dtype, int U, int I,
                      double* vf_out, int* status);
 
 /*
+ * ffca_fastfca_run plus its final statistics refresh -- the whole of
+ * fastfca.run_fastfca (fastfca.py:401-474, stats at :466 via _stats_refresh
+ * :373-387): after the loop kernel the per-point refresh runs on the
+ * device-resident final state; mu_out (U, J, N, F, I) complex, phi_out
+ * (U, J, N, F, I) real, either may be NULL.  Host mode moves both outputs
+ * chunk by chunk, overlapped with the next chunk's loop.
+ */
+int ffca_fastfca_run_stats(int device, void* stream, int mem, int dtype, int U, int I, int J, int N, int F,
+                           const void* y, const void* P0, const void* lam0, const void* v0, int vf_mode,
+                           double vf_scalar, const void* vf, int iterations, int inner_iterations,
+                           int record_likelihood, void* P_out, void* lam_out, void* v_out, double* ll_out,
+                           double* vf_out, int* status, void* mu_out, void* phi_out);
+
+/*
  * Transformed posterior statistics at (P, lam, v): mu_t = g * P^H y and
  * phi_t = max(a (1 - g), 0) with a = v lam, g = a / w.
  * Replaces fastfca._stats_refresh (fastfca.py:373-387) and, given y_t,

@@ -49,6 +49,8 @@ SIGNATURES = {
     "ffca_plan_loop": [_i, _i, _i, _i, _i, _i, _i, _i, _ip],
     "ffca_fastfca_run": [_i, _vp, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _i, _d, _vp, _i, _i, _i,
                          _vp, _vp, _vp, _vp, _vp, _vp],
+    "ffca_fastfca_run_stats": [_i, _vp, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _i, _d, _vp, _i, _i, _i,
+                               _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "ffca_fastfca_stats": [_i, _vp, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp],
     "ffca_fastfca_images": [_i, _vp, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp],
     "ffca_back_transform": [_i, _vp, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp],

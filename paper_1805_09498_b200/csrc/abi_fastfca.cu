@@ -7,6 +7,7 @@
 
 #include "ffca_loop.cuh"
 #include "host_common.h"
+#include "points.h"
 
 namespace ffca {
 
@@ -89,15 +90,21 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
   // spreads the bins over more SMs (four such CTAs fit an SM).  Measured: config 0 (513 bins)
   // kernel 0.203 -> 0.197 ms; for complex64 the 4-bin CTAs stay faster (one config-3 mixture
   // 0.109 vs 0.113 ms, two 0.161 vs 0.195 ms), so complex64 keeps G0.
-  if (dtype == FFCA_C128 && G0 > 1 && I <= 4 && (total_bins + G0 - 1) / G0 < 2LL * nsm) {
-    fill(1, 1, true);
-    if (p.threads > 128) {
-      p.threads = 128;
-      LoopSmem L(I, J, JM, 1, p.NL, 4, rsz, vf_mode, true, VMAX);
+  // The one-bin CTA has half the threads of the G0 = 2 plan -- the same frame slots -- and reduces
+  // over 16-lane segments (ffca_loop.cuh bin_reduce), so both plans give bitwise the same bins:
+  // results do not depend on the batch size, the host pipeline's chunking or the shard a bin is in.
+  if (dtype == FFCA_C128 && G0 == 2 && I <= 4 && (total_bins + G0 - 1) / G0 < 2LL * nsm) {
+    fill(G0, 1, true);
+    const int t2 = p.threads;
+    const bool fits2 = p.slab <= kSlabBudget && p.smem <= smem_optin;
+    if (fits2 && t2 >= 128) {
+      fill(1, 1, true);
+      p.threads = t2 / 2;
+      LoopSmem L(I, J, JM, 1, p.NL, p.threads / 32, rsz, vf_mode, true, VMAX);
       p.L = L;
       p.smem = L.total;
+      if (p.slab <= kSlabBudget && p.smem <= smem_optin) return FFCA_OK;
     }
-    if (p.slab <= kSlabBudget && p.smem <= smem_optin) return FFCA_OK;
   }
   // complex64, I = J = 3: 2-bin CTAs of 128 threads (64 per bin, as in the 4-bin / 256-thread
   // CTAs) -- four CTAs per SM instead of two overlap each other's reductions and solves better.
@@ -184,6 +191,7 @@ struct DevProblem {
   double* vf_out;
   double* ll_bins;  // (U*F, nev) or null
   int* status;      // (U*F)
+  void *mu, *phi;   // optional: statistics refresh at the final state (U,J,N,F,I), fastfca.py:373-387
 };
 
 static int launch_problem(int device, const DevProblem& d, cudaStream_t s) {
@@ -272,6 +280,15 @@ static int launch_problem(int device, const DevProblem& d, cudaStream_t s) {
   }
   if (scratch) FFCA_CK(cudaFreeAsync(scratch, s));
   if (packed) FFCA_CK(cudaFreeAsync(packed, s));
+  if (d.mu || d.phi) {
+    // run_fastfca's _stats_refresh (fastfca.py:466, 373-387) on the loop's final state, from the
+    // device copies of y and (P, lambda, v) this call already holds
+    PointArgs pa = {};
+    pa.mode = PM_STATS; pa.U = d.U; pa.I = d.I; pa.J = d.J; pa.N = d.N; pa.F = d.F;
+    pa.y = d.y; pa.P = d.P; pa.lam = d.lam; pa.v = d.v;
+    pa.out0 = d.mu; pa.out1 = d.phi;
+    FFCA_TRY(launch_points(d.dtype, pa, s));
+  }
   return FFCA_OK;
 }
 
@@ -309,46 +326,54 @@ static int copy_blk(void* dst, const void* src, const Blk& b, int U, int F, int 
 // device buffer sets).  Chunks are mixture blocks (U > 1) or frequency
 // blocks of a single mixture; bins are independent, so the results are
 // bitwise those of one launch.
-static int pipelined_host_run(int device, cudaStream_t user, const DevProblem& proto, bool rec, int nchunk,
-                              bool by_mixture,
-                              const void* y, const void* P0, const void* lam0, const void* v0, const void* vf,
-                              void* P_out, void* lam_out, void* v_out, double* ll_out, double* vf_out,
-                              int* status_out) {
+// Streams, events and device buffers of one pipelined call: created by the body, released by
+// pipelined_host_run on every path (success or any failure inside the body).
+struct PipeRes {
+  cudaStream_t sin = nullptr, scomp = nullptr, sout = nullptr;
+  cudaEvent_t start = nullptr, ev_in[2] = {nullptr, nullptr}, ev_k[2] = {nullptr, nullptr},
+              ev_out[2] = {nullptr, nullptr};
+  std::vector<void*> allocs;
+};
+
+static int pipelined_body(PipeRes& R, int device, cudaStream_t user, const DevProblem& proto, bool rec, int nchunk,
+                          bool by_mixture,
+                          const void* y, const void* P0, const void* lam0, const void* v0, const void* vf,
+                          void* P_out, void* lam_out, void* v_out, double* ll_out, double* vf_out,
+                          int* status_out, void* mu_out, void* phi_out) {
   const int U = proto.U, I = proto.I, J = proto.J, N = proto.N, F = proto.F;
   const size_t rs = rsize(proto.dtype), cs = csize(proto.dtype);
   const long long nb = (long long)U * F;
   const int nev = 1 + 2 * proto.iters;
   const Blk By{size_t(I) * N, 1, cs}, BP{1, size_t(I) * I, cs}, Bl{size_t(J), size_t(I), rs},
-      Bv{size_t(J) * N, 1, rs}, Bvb{1, 1, rs}, Bvo{1, 1, 8}, Bst{1, 1, 4}, Bll{1, size_t(nev), 8};
+      Bv{size_t(J) * N, 1, rs}, Bvb{1, 1, rs}, Bvo{1, 1, 8}, Bst{1, 1, 4}, Bll{1, size_t(nev), 8},
+      Bmu{size_t(J) * N, size_t(I), cs}, Bphi{size_t(J) * N, size_t(I), rs};
   const int cu = by_mixture ? (U + nchunk - 1) / nchunk : 1;
   const int cf = by_mixture ? F : (F + nchunk - 1) / nchunk;
   auto bytes = [&](const Blk& b) { return size_t(cu) * b.A * cf * b.B * b.es; };
 
-  cudaStream_t sin, scomp, sout;
-  FFCA_CK(cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking));
-  FFCA_CK(cudaStreamCreateWithFlags(&scomp, cudaStreamNonBlocking));
-  FFCA_CK(cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking));
-  cudaEvent_t start;
-  FFCA_CK(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
-  FFCA_CK(cudaEventRecord(start, user));  // order after prior work on the caller's stream
-  FFCA_CK(cudaStreamWaitEvent(sin, start, 0));
-  cudaEvent_t ev_in[2], ev_k[2], ev_out[2];
+  FFCA_CK(cudaStreamCreateWithFlags(&R.sin, cudaStreamNonBlocking));
+  FFCA_CK(cudaStreamCreateWithFlags(&R.scomp, cudaStreamNonBlocking));
+  FFCA_CK(cudaStreamCreateWithFlags(&R.sout, cudaStreamNonBlocking));
+  cudaStream_t sin = R.sin, scomp = R.scomp, sout = R.sout;
+  FFCA_CK(cudaEventCreateWithFlags(&R.start, cudaEventDisableTiming));
+  FFCA_CK(cudaEventRecord(R.start, user));  // order after prior work on the caller's stream
+  FFCA_CK(cudaStreamWaitEvent(sin, R.start, 0));
+  cudaEvent_t *ev_in = R.ev_in, *ev_k = R.ev_k, *ev_out = R.ev_out;
   for (int k = 0; k < 2; ++k) {
     FFCA_CK(cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming));
     FFCA_CK(cudaEventCreateWithFlags(&ev_k[k], cudaEventDisableTiming));
     FFCA_CK(cudaEventCreateWithFlags(&ev_out[k], cudaEventDisableTiming));
   }
   // device buffers: two slots of chunk inputs/outputs + full status / ll
-  std::vector<void*> allocs;
   auto dalloc = [&](size_t n, void** p) -> int {
     *p = nullptr;
     if (n == 0) return FFCA_OK;
     FFCA_CK(cudaMallocAsync(p, n, sin));
-    allocs.push_back(*p);
+    R.allocs.push_back(*p);
     return FFCA_OK;
   };
   void *dy[2], *dP0[2], *dl0[2], *dv0[2], *dvf[2] = {nullptr, nullptr}, *dP[2], *dl[2], *dv[2], *dvo[2] = {nullptr, nullptr},
-       *dst[2], *dll[2] = {nullptr, nullptr};
+       *dst[2], *dll[2] = {nullptr, nullptr}, *dmu[2] = {nullptr, nullptr}, *dphi[2] = {nullptr, nullptr};
   int rc = FFCA_OK;
   void *fstatus = nullptr, *fll = nullptr, *llmix = nullptr;
   if (!rc) rc = dalloc(size_t(nb) * 4, &fstatus);
@@ -381,6 +406,8 @@ static int pipelined_host_run(int device, cudaStream_t user, const DevProblem& p
     if (!rc && vf_out) rc = dalloc(bytes(Bvo), &dvo[k]);
     if (!rc && !by_mixture) rc = dalloc(bytes(Bst), &dst[k]);
     if (!rc && rec && !by_mixture) rc = dalloc(bytes(Bll), &dll[k]);
+    if (!rc && mu_out) rc = dalloc(bytes(Bmu), &dmu[k]);
+    if (!rc && phi_out) rc = dalloc(bytes(Bphi), &dphi[k]);
   }
   int nch = 0;
   for (int c0 = 0; !rc && c0 < (by_mixture ? U : F); c0 += (by_mixture ? cu : cf), ++nch) {
@@ -406,6 +433,7 @@ static int pipelined_host_run(int device, cudaStream_t user, const DevProblem& p
     d.F = Fc;
     d.y = dy[k]; d.v0 = dv0[k]; d.vf = dvf[k];
     d.v = dv[k]; d.vf_out = (double*)dvo[k];
+    d.mu = dmu[k]; d.phi = dphi[k];
     if (by_mixture) {  // views into the whole-batch buffers (mixture blocks are contiguous)
       const size_t b0 = size_t(u0) * F;
       d.P0 = (const char*)fP0 + b0 * I * I * cs;
@@ -440,6 +468,8 @@ static int pipelined_host_run(int device, cudaStream_t user, const DevProblem& p
     }
     if (!rc) rc = copy_blk(v_out, dv[k], Bv, U, F, u0, Uc, f0, Fc, false, sout);
     if (!rc && vf_out) rc = copy_blk(vf_out, dvo[k], Bvo, U, F, u0, Uc, f0, Fc, false, sout);
+    if (!rc && mu_out) rc = copy_blk(mu_out, dmu[k], Bmu, U, F, u0, Uc, f0, Fc, false, sout);
+    if (!rc && phi_out) rc = copy_blk(phi_out, dphi[k], Bphi, U, F, u0, Uc, f0, Fc, false, sout);
     if (!rc) FFCA_CK(cudaEventRecord(ev_out[k], sout));
   }
   if (!rc && by_mixture) {  // the whole-batch P / lambda after the last kernel
@@ -456,17 +486,31 @@ static int pipelined_host_run(int device, cudaStream_t user, const DevProblem& p
     if (!rc) rc = finish_status((const int*)fstatus, status_out, nb, FFCA_MEM_HOST, scomp,
                                 FFCA_ST_SINGULAR_P | FFCA_ST_SINGULAR_B);
   }
-  for (void* q : allocs) cudaFreeAsync(q, scomp);
-  cudaStreamSynchronize(scomp);
-  for (int k = 0; k < 2; ++k) {
-    cudaEventDestroy(ev_in[k]);
-    cudaEventDestroy(ev_k[k]);
-    cudaEventDestroy(ev_out[k]);
-  }
-  cudaEventDestroy(start);
-  cudaStreamDestroy(sin);
-  cudaStreamDestroy(scomp);
-  cudaStreamDestroy(sout);
+  return rc;
+}
+
+static int pipelined_host_run(int device, cudaStream_t user, const DevProblem& proto, bool rec, int nchunk,
+                              bool by_mixture,
+                              const void* y, const void* P0, const void* lam0, const void* v0, const void* vf,
+                              void* P_out, void* lam_out, void* v_out, double* ll_out, double* vf_out,
+                              int* status_out, void* mu_out, void* phi_out) {
+  PipeRes R;
+  const int rc = pipelined_body(R, device, user, proto, rec, nchunk, by_mixture, y, P0, lam0, v0, vf, P_out,
+                                lam_out, v_out, ll_out, vf_out, status_out, mu_out, phi_out);
+  // Every path ends here.  Drain all three streams first: after a failure, H2D copies on sin and
+  // D2H copies on sout may still be reading / writing the caller's host buffers and the device
+  // buffers freed below.
+  for (cudaStream_t q : {R.sin, R.scomp, R.sout})
+    if (q) cudaStreamSynchronize(q);
+  for (void* q : R.allocs) cudaFreeAsync(q, R.scomp);
+  if (R.scomp) cudaStreamSynchronize(R.scomp);
+  for (int k = 0; k < 2; ++k)
+    for (cudaEvent_t e : {R.ev_in[k], R.ev_k[k], R.ev_out[k]})
+      if (e) cudaEventDestroy(e);
+  if (R.start) cudaEventDestroy(R.start);
+  for (cudaStream_t q : {R.sin, R.scomp, R.sout})
+    if (q) cudaStreamDestroy(q);
+  if (rc != FFCA_OK) cudaGetLastError();  // the error is reported through rc / ffca_last_error
   return rc;
 }
 
@@ -474,7 +518,8 @@ static int loop_entry(int device, void* stream, int mem, int dtype, int U, int I
                       const void* y, const void* P0, const void* lam0, const void* v0, int vf_mode,
                       double vf_scalar, const void* vf, int iterations, int inner_iterations,
                       int record_likelihood, void* P_out, void* lam_out, void* v_out, double* ll_out,
-                      double* vf_out, int* status, int p_only) {
+                      double* vf_out, int* status, int p_only, void* mu_out = nullptr,
+                      void* phi_out = nullptr) {
   reset_launches();
   if (!check_dims(dtype, U, I, J, N, F)) return FFCA_E_ARG;
   if (I > 8 || J > 8) {
@@ -506,7 +551,8 @@ static int loop_entry(int device, void* stream, int mem, int dtype, int U, int I
   d.iters = iterations; d.K = inner_iterations; d.p_only = p_only;
 
   // host mode with a large input: pipeline H2D / compute / D2H over chunks
-  const size_t in_bytes = size_t(U) * I * N * F * cs + size_t(U) * J * N * F * rs;
+  const size_t in_bytes = size_t(U) * I * N * F * cs + size_t(U) * J * N * F * rs +
+                          (mu_out ? size_t(U) * J * N * F * I * cs : 0) + (phi_out ? size_t(U) * J * N * F * I * rs : 0);
   // FFCA_NO_PIPELINE=1 disables, FFCA_PIPELINE_MIN_BYTES overrides the threshold (tests)
   const char* nopipe = getenv("FFCA_NO_PIPELINE");
   const char* minb = getenv("FFCA_PIPELINE_MIN_BYTES");
@@ -520,7 +566,7 @@ static int loop_entry(int device, void* stream, int mem, int dtype, int U, int I
     const int nchunk = by_mix ? std::min(U, want) : std::min(F, want);
     if (nchunk >= 2) {
       return pipelined_host_run(device, s, d, record_likelihood != 0, nchunk, by_mix, y, P0, lam0, v0, vf, P_out, lam_out, v_out,
-                                record_likelihood ? ll_out : nullptr, vf_out, status);
+                                record_likelihood ? ll_out : nullptr, vf_out, status, mu_out, phi_out);
     }
   }
 
@@ -537,6 +583,8 @@ static int loop_entry(int device, void* stream, int mem, int dtype, int U, int I
   FFCA_TRY(st.out(v_out, size_t(U) * J * N * F * rs, &ov));
   if (vf_out) FFCA_TRY(st.out(vf_out, size_t(nb) * 8, &ovf));
   if (record_likelihood && ll_out) FFCA_TRY(st.out(ll_out, size_t(U) * nev * 8, &oll));
+  FFCA_TRY(st.out(mu_out, size_t(U) * J * N * F * I * cs, &d.mu));
+  FFCA_TRY(st.out(phi_out, size_t(U) * J * N * F * I * rs, &d.phi));
   void *dstatus, *dllb = nullptr;
   FFCA_TRY(st.scratch(size_t(nb) * 4, &dstatus));
   FFCA_CK(cudaMemsetAsync(dstatus, 0, size_t(nb) * 4, s));
@@ -558,6 +606,20 @@ extern "C" int ffca_fastfca_run(int device, void* stream, int mem, int dtype, in
   return loop_entry(device, stream, mem, dtype, U, I, J, N, F, y, P0, lam0, v0, vf_mode, vf_scalar, vf,
                     iterations, inner_iterations, record_likelihood, P_out, lam_out, v_out, ll_out, vf_out,
                     status, 0);
+}
+
+// run_fastfca including its final statistics refresh (fastfca.py:466): the loop kernel, then the
+// per-point refresh on the device-resident final state; mu_out (U,J,N,F,I) complex and phi_out
+// (U,J,N,F,I) real (either may be null).  Host mode pipelines both outputs' D2H with the chunks.
+extern "C" int ffca_fastfca_run_stats(int device, void* stream, int mem, int dtype, int U, int I, int J, int N,
+                                      int F, const void* y, const void* P0, const void* lam0, const void* v0,
+                                      int vf_mode, double vf_scalar, const void* vf, int iterations,
+                                      int inner_iterations, int record_likelihood, void* P_out, void* lam_out,
+                                      void* v_out, double* ll_out, double* vf_out, int* status, void* mu_out,
+                                      void* phi_out) {
+  return loop_entry(device, stream, mem, dtype, U, I, J, N, F, y, P0, lam0, v0, vf_mode, vf_scalar, vf,
+                    iterations, inner_iterations, record_likelihood, P_out, lam_out, v_out, ll_out, vf_out,
+                    status, 0, mu_out, phi_out);
 }
 
 // fastfca.log_likelihood (fastfca.py:240-255): the loop kernel with zero
@@ -657,8 +719,13 @@ extern "C" int ffca_plan_loop(int device, int dtype, int U, int I, int J, int N,
     cudaGetLastError();
     optin = 232448;
   }
+  int nsm = 148;
+  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
+    cudaGetLastError();
+    nsm = 148;
+  }
   LoopPlan p;
-  int rc = plan_loop(dtype, I, J, N, (long long)U * F, vf_mode, p, size_t(optin));
+  int rc = plan_loop(dtype, I, J, N, (long long)U * F, vf_mode, p, size_t(optin), nsm);
   out6[0] = p.G;
   out6[1] = p.C;
   out6[2] = p.NL;

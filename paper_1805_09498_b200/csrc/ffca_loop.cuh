@@ -135,7 +135,8 @@ struct LoopSmem {
     bst = o;   // unused (the solves read the reduced sums in tot)
     {  // solver workspace: per-system matrices (I <= 4) or B_i^-1 + group rows (I > 4)
       const size_t m1 = size_t(G) * (I + 1) * I * I * 16, m2 = (size_t(I) * I * I + 2 * I * (loop_pgroup(I) + 1)) * 16;
-      size_t wp = align16(size_t(W) * G * VMAX * rsz);  // warp partials in the compute type
+      const int nseg = (G == 1 && !ilv && rsz == 8) ? 2 : 1;  // 16-lane segments (bin_reduce SEG)
+      size_t wp = align16(size_t(W) * nseg * G * VMAX * rsz);  // warp partials in the compute type
       const size_t ms = align16(m1 > m2 ? m1 : m2);
       if (ilv) {  // I > 4 phase B: per-warp buffers of 32 frames' reciprocal weights
         const size_t wb = size_t(W) * 32 * ((I + 3) & ~3) * rsz;
@@ -199,8 +200,9 @@ __device__ __forceinline__ T bin_warp_sum(T x) {
 // ranks in rank order, into tot[g*VMAX + k].
 template <int G, typename T>
 __device__ __forceinline__ void bin_reduce_tail(int nv, const T* wpart, double* cpart, double* tot, int C, int VMAX,
-                                                int& parity) {
-  const int tid = threadIdx.x, W = blockDim.x >> 5;
+                                                int& parity, int W = -1) {
+  const int tid = threadIdx.x;
+  if (W < 0) W = blockDim.x >> 5;  // rows of warp partials per bin
   __syncthreads();
   double* cp = cpart + parity * G * VMAX;
   double* dst = (C > 1) ? cp : tot;
@@ -241,14 +243,21 @@ __device__ __forceinline__ void halving_step(R (&buf)[N], int lane, int& base) {
 }
 
 // Warp half of the reduction as a transposed (halving) butterfly over the
-// L = 32/G lanes of a bin: at each step a lane keeps one half of its current
-// values and receives the partner's copy of that half, so the V values take
-// ~V shuffles instead of V*log2(L).  Lane with in-bin bits (b16..bG) ends up
+// L = SEG lanes of a bin segment: at each step a lane keeps one half of its
+// current values and receives the partner's copy of that half, so the V values
+// take ~V shuffles instead of V*log2(L).  Lane with in-bin bits (b..bG) ends up
 // owning values [base, base + V2/L), base = sum_s b_s * V2 / 2^(s+1).
-template <typename R, int V, int G, typename T>
+// SEG = 32/G is one segment per warp and bin.  SEG = 16 at G = 1 splits every
+// warp into two "virtual warps" of 16 frame slots: the sum tree is then exactly
+// that of the G = 2 plan with twice the threads (16 lanes per bin, warps in
+// slot order), so a bin's results do not depend on which of the two plans a
+// batch size selects (complex128, abi_fastfca.cu plan_loop).
+template <typename R, int V, int G, int SEG = 32 / G, typename T>
 __device__ __forceinline__ void bin_reduce(const R (&vals)[V], T* wpart, double* cpart, double* tot, int C,
                                            int VMAX, int& parity) {
-  constexpr int L = 32 / G;
+  constexpr int L = SEG;
+  constexpr int NSEG = 32 / (G * SEG);  // segments per warp and bin
+  static_assert(NSEG >= 1 && NSEG * G * SEG == 32, "segments tile the warp");
   constexpr int V2 = (V + L - 1) / L * L;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane % G;
@@ -256,12 +265,13 @@ __device__ __forceinline__ void bin_reduce(const R (&vals)[V], T* wpart, double*
 #pragma unroll
   for (int k = 0; k < V2; ++k) buf[k] = k < V ? vals[k] : R(0);
   int base = 0;
-  halving_step<R, V2, 16, G>(buf, lane, base);
-  T* row = wpart + (warp * G + g) * VMAX;  // warp partials (the loop kernel keeps them in its compute type)
+  halving_step<R, V2, G * SEG / 2, G>(buf, lane, base);
+  const int vw = warp * NSEG + lane / (G * SEG);  // (virtual) warp row in slot order
+  T* row = wpart + (vw * G + g) * VMAX;  // warp partials (the loop kernel keeps them in its compute type)
 #pragma unroll
   for (int k = 0; k < V2 / L; ++k)
     if (base + k < V) row[base + k] = T(buf[k]);
-  bin_reduce_tail<G>(V, wpart, cpart, tot, C, VMAX, parity);
+  bin_reduce_tail<G>(V, wpart, cpart, tot, C, VMAX, parity, (int(blockDim.x) >> 5) * NSEG);
 }
 
 // 3 x 3 determinant of the rows r0 < r1 < r2 and columns c0 < c1 < c2 of a row-major 4 x 4 matrix.
@@ -917,6 +927,8 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
   const int tid = threadIdx.x;
   const int g = tid % G;
   const int slot = tid / G, nslots = blockDim.x / G;
+  // complex128 one-bin CTAs reduce over 16-lane segments (bin_reduce): bitwise the G = 2 plan
+  constexpr int SEG = (G == 1 && I <= 4 && sizeof(R) == 8) ? 16 : 32 / G;
 
   extern __shared__ __align__(16) unsigned char smem[];
   const int W = blockDim.x >> 5;
@@ -1058,7 +1070,7 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
           psum += z.x * z.x + z.y * z.y;
         }
     const R pv[1] = {psum};
-    bin_reduce<R, 1, G>(pv, wpart, cpart, tot, C, VMAX, parity);
+    bin_reduce<R, 1, G, SEG>(pv, wpart, cpart, tot, C, VMAX, parity);
     if (tid < G) {
       const double mean = tot[tid * VMAX] / (double(I) * double(N));
       const double fl = fmax(1e-10 * mean, double(Floors<R>::vmin));
@@ -1139,7 +1151,7 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
         }
       }
       FFCA_PROBE(0)
-      bin_reduce<R, VA, G>(acc, wpart, cpart, tot, C, VMAX, parity);
+      bin_reduce<R, VA, G, SEG>(acc, wpart, cpart, tot, C, VMAX, parity);
       FFCA_PROBE(1)
       if (rec && tid < G) llA = tot[tid * VMAX + VA - 1];
       // ---------------- lambda' per (bin, source) (fastfca.py:341-345) -------
@@ -1222,7 +1234,7 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
       if (rec && ch == 0) pw.template phaseB<true>(acc, ch);
       else pw.template phaseB<false>(acc, ch);
       FFCA_PROBE(3)
-      bin_reduce<R, NB + 1, G>(acc, wpart, cpart, tot, C, VMAX, parity);
+      bin_reduce<R, NB + 1, G, SEG>(acc, wpart, cpart, tot, C, VMAX, parity);
       if (rec && ch == 0 && tid < G) llB = tot[tid * VMAX + NB];
     }
     }
@@ -1395,7 +1407,7 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
     pw.load_PL();
     R acc[1] = {R(0)};
     pw.phaseL(acc);
-    bin_reduce<R, 1, G>(acc, wpart, cpart, tot, C, VMAX, parity);
+    bin_reduce<R, 1, G, SEG>(acc, wpart, cpart, tot, C, VMAX, parity);
     if (tid < G) {
       const long long b = group * G + tid;
       double2* Ms = Msys + (tid * (I + 1)) * I * I;

@@ -72,52 +72,18 @@ class FastFcaParams:
         return FastFcaParams(self.P.copy(), self.Lam.copy(), self.v.copy())
 
 
+@dataclass
 class TransformedStats:
     """Posterior statistics in the transformed basis (fastfca.py:87-96).
 
     ``mu`` (J, N, F, I) complex holds P^H mu_j and ``phi`` (J, N, F, I) real the
-    diagonal of P^H Phi_j P.  Statistics returned by ``run_fastfca`` are
-    materialised lazily on first access (one device pass over y); until then
-    ``mmse_images_fastfca`` computes images straight from the final state
-    without forming mu_t.
+    diagonal of P^H Phi_j P.  ``run_fastfca`` fills them at the final state in
+    the same device call as the loop (fastfca.py:466), so they are a snapshot:
+    later changes to ``run.params`` do not touch them.
     """
 
-    def __init__(self, mu=None, phi=None, *, source=None):
-        self._mu = mu
-        self._phi = phi
-        self._source = source  # (ObservationTensor, FastFcaParams) when lazy
-
-    def _materialize(self):
-        obs, params = self._source
-        mu, phi = _stats(obs, params, want_mu=self._mu is None, want_phi=self._phi is None)
-        if self._mu is None:
-            self._mu = mu
-        if self._phi is None:
-            self._phi = phi
-
-    @property
-    def mu(self) -> np.ndarray:
-        if self._mu is None and self._source is not None:
-            self._materialize()
-        return self._mu
-
-    @mu.setter
-    def mu(self, value):
-        self._mu = value
-
-    @property
-    def phi(self) -> np.ndarray:
-        if self._phi is None and self._source is not None:
-            self._materialize()
-        return self._phi
-
-    @phi.setter
-    def phi(self, value):
-        self._phi = value
-
-    @property
-    def is_lazy(self) -> bool:
-        return self._source is not None and (self._mu is None or self._phi is None)
+    mu: np.ndarray
+    phi: np.ndarray
 
 
 @dataclass
@@ -187,8 +153,9 @@ def run_fastfca(
     """Hybrid estimation loop on the GPU (fastfca.py:401-474).
 
     One EM sweep on (v, Lambda), then the fixed-point update of P, per outer
-    iteration -- the whole loop is one kernel launch.  Returns the final
-    parameters, lazily refreshed transformed statistics and counters; with
+    iteration -- the whole loop is one kernel launch, followed by the statistics
+    refresh in the same call.  Returns the final parameters, the transformed
+    statistics at the final state and counters; with
     ``record_likelihood`` the likelihood at init, after every EM sweep and
     after every P update.
     """
@@ -206,18 +173,21 @@ def run_fastfca(
     P = np.empty_like(P0)
     lam = np.empty_like(lam0)
     v = np.empty_like(v0)
+    mu = np.empty((J, N, F, I), y.dtype)
+    phi = np.empty((J, N, F, I), v0.dtype)
     nev = 1 + 2 * int(iterations)
     ll = np.empty((1, nev)) if record_likelihood else None
-    rc = lib.ffca_fastfca_run(_lib.device(), None, _lib.MEM_HOST, code, 1, I, J, N, F,
-                              _lib.ptr(y), _lib.ptr(P0), _lib.ptr(lam0), _lib.ptr(v0),
-                              mode, vf_scalar, _lib.ptr(vf_arr), int(iterations), int(inner_iterations),
-                              1 if record_likelihood else 0, _lib.ptr(P), _lib.ptr(lam), _lib.ptr(v),
-                              _lib.ptr(ll), None, None)
-    _lib.check(rc, "ffca_fastfca_run")
+    # the loop and the final statistics refresh (fastfca.py:466) in one device call
+    rc = lib.ffca_fastfca_run_stats(_lib.device(), None, _lib.MEM_HOST, code, 1, I, J, N, F,
+                                    _lib.ptr(y), _lib.ptr(P0), _lib.ptr(lam0), _lib.ptr(v0),
+                                    mode, vf_scalar, _lib.ptr(vf_arr), int(iterations), int(inner_iterations),
+                                    1 if record_likelihood else 0, _lib.ptr(P), _lib.ptr(lam), _lib.ptr(v),
+                                    _lib.ptr(ll), None, None, _lib.ptr(mu), _lib.ptr(phi))
+    _lib.check(rc, "ffca_fastfca_run_stats")
     params = FastFcaParams(P=P, Lam=lam, v=v)
     counters = OpCounters()
     counters.add_inversions(int(iterations) * (I + 1) * F * int(inner_iterations))
-    run = FastFcaRun(params=params, stats=TransformedStats(source=(obs, params)), counters=counters)
+    run = FastFcaRun(params=params, stats=TransformedStats(mu=mu, phi=phi), counters=counters)
     if record_likelihood:
         T = int(iterations)
         run.loglik_init = float(ll[0, 0])
@@ -227,20 +197,35 @@ def run_fastfca(
 
 
 def run_fastfca_batch(y, P0, lam0, v0, iterations=20, inner_iterations=1, v_floor=None,
-                      record_likelihood=False, stream=None, out=None):
+                      record_likelihood=False, stream=None, out=None, stats=False, stats_out=None):
     """Batched extension: U independent mixtures in one launch.
 
     y (U, I, N, F), P0 (U, F, I, I), lam0 (U, J, F, I), v0 (U, J, N, F);
     v_floor None (per-mixture power floor) / scalar / (U, F).  Returns
-    (P, lam, v, ll (U, 1+2T) or None).  Numpy arrays only.
+    (P, lam, v, ll (U, 1+2T) or None); with ``stats`` also (mu, phi), each
+    (U, J, N, F, I) -- run_fastfca's final refresh for every mixture.  Numpy
+    arrays only.
     """
-    lib = _lib.require_gpu()
+    y = np.asarray(y)
+    if not np.iscomplexobj(y) or y.ndim != 4:
+        raise DimensionMismatch(f"y must be a complex (U, I, N, F) array, got {y.dtype} {y.shape}")
     c64 = y.dtype == np.complex64
     code = _lib.C64 if c64 else _lib.C128
+    # every array in the precision the kernel runs in (y's): the C ABI reads them as such
+    y = _as_c(y, c64)
+    P0, lam0, v0 = _as_c(P0, c64), _as_r(lam0, c64), _as_r(v0, c64)
     U, I, N, F = y.shape
-    J = v0.shape[1]
+    J = v0.shape[1] if v0.ndim == 4 else -1
     if P0.shape != (U, F, I, I) or lam0.shape != (U, J, F, I) or v0.shape != (U, J, N, F):
         raise DimensionMismatch("batched shapes disagree")
+    if out is not None:
+        out = tuple(out)
+        if len(out) != 3:
+            raise ValueError("out must be (P, lam, v)")
+        for o, ref, name in zip(out, (P0, lam0, v0), ("P", "lam", "v")):
+            if (not isinstance(o, np.ndarray) or o.shape != ref.shape or o.dtype != ref.dtype
+                    or not o.flags.c_contiguous or not o.flags.writeable):
+                raise ValueError(f"out {name} must be a writeable C-contiguous {ref.dtype} array of shape {ref.shape}")
     if v_floor is None:
         mode, vfs, vfa = _lib.VF_AUTO, 0.0, None
     elif np.ndim(v_floor) == 0:
@@ -249,11 +234,25 @@ def run_fastfca_batch(y, P0, lam0, v0, iterations=20, inner_iterations=1, v_floo
         mode, vfs, vfa = _lib.VF_BIN, 0.0, _as_r(np.reshape(v_floor, (U, F)), c64)
     P, lam, v = out if out is not None else (np.empty_like(P0), np.empty_like(lam0), np.empty_like(v0))
     ll = np.empty((U, 1 + 2 * iterations)) if record_likelihood else None
-    rc = lib.ffca_fastfca_run(_lib.device(), stream, _lib.MEM_HOST, code, U, I, J, N, F,
-                              _lib.ptr(y), _lib.ptr(P0), _lib.ptr(lam0), _lib.ptr(v0), mode, vfs,
-                              _lib.ptr(vfa), iterations, inner_iterations, 1 if record_likelihood else 0,
-                              _lib.ptr(P), _lib.ptr(lam), _lib.ptr(v), _lib.ptr(ll), None, None)
-    _lib.check(rc, "ffca_fastfca_run")
+    mu = phi = None
+    if stats:
+        if stats_out is not None:
+            mu, phi = stats_out
+            for o, shape, dt in ((mu, (U, J, N, F, I), y.dtype), (phi, (U, J, N, F, I), v0.dtype)):
+                if (not isinstance(o, np.ndarray) or o.shape != shape or o.dtype != dt or not o.flags.c_contiguous
+                        or not o.flags.writeable):
+                    raise ValueError(f"stats_out must be writeable C-contiguous {dt} arrays of shape {shape}")
+        else:
+            mu, phi = np.empty((U, J, N, F, I), y.dtype), np.empty((U, J, N, F, I), v0.dtype)
+    lib = _lib.require_gpu()
+    rc = lib.ffca_fastfca_run_stats(_lib.device(), stream, _lib.MEM_HOST, code, U, I, J, N, F,
+                                    _lib.ptr(y), _lib.ptr(P0), _lib.ptr(lam0), _lib.ptr(v0), mode, vfs,
+                                    _lib.ptr(vfa), iterations, inner_iterations, 1 if record_likelihood else 0,
+                                    _lib.ptr(P), _lib.ptr(lam), _lib.ptr(v), _lib.ptr(ll), None, None,
+                                    _lib.ptr(mu), _lib.ptr(phi))
+    _lib.check(rc, "ffca_fastfca_run_stats")
+    if stats:
+        return P, lam, v, ll, mu, phi
     return P, lam, v, ll
 
 

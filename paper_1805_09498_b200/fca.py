@@ -67,43 +67,16 @@ class FcaParams:
         return FcaParams(self.S.copy(), self.v.copy())
 
 
+@dataclass
 class PosteriorStats:
     """Posterior means (J, N, F, I) and covariances (J, N, F, I, I) (fca.py:63-66).
 
-    ``run_fca`` returns them lazily: they are the E-step at the parameters
-    of the last sweep, recomputed on device on first access.
+    ``run_fca`` returns the last sweep's E-step (at the penultimate parameters,
+    which the loop kernel writes out), computed in the same call.
     """
 
-    def __init__(self, mu=None, phi=None, *, source=None):
-        self._mu, self._phi, self._source = mu, phi, source
-
-    def _materialize(self):
-        params, obs = self._source
-        st = e_step(params, obs)
-        if self._mu is None:
-            self._mu = st.mu
-        if self._phi is None:
-            self._phi = st.phi
-
-    @property
-    def mu(self):
-        if self._mu is None and self._source is not None:
-            self._materialize()
-        return self._mu
-
-    @mu.setter
-    def mu(self, value):
-        self._mu = value
-
-    @property
-    def phi(self):
-        if self._phi is None and self._source is not None:
-            self._materialize()
-        return self._phi
-
-    @phi.setter
-    def phi(self, value):
-        self._phi = value
+    mu: np.ndarray
+    phi: np.ndarray
 
 
 @dataclass
@@ -214,7 +187,7 @@ def run_fca(
     """E and M steps for ``iterations`` sweeps in one device launch.  fca.py:187-215.
 
     ``stats`` are those of the last sweep's E-step (at the penultimate
-    parameters), materialised lazily; None when iterations == 0, in which case
+    parameters); None when iterations == 0, in which case
     ``params is init`` as in the reference.
     """
     _check(init, obs)
@@ -237,7 +210,7 @@ def run_fca(
                                 _lib.ptr(ll), None), "ffca_fca_run")
     counters.add_inversions(iterations * (J + N) * F)
     counters.add_matmuls(iterations * 2 * J * N * F)
-    stats = PosteriorStats(source=(FcaParams(Sp, vp), obs))
+    stats = e_step(FcaParams(Sp, vp), obs)  # fca.py:211: the last sweep's E-step statistics
     hist = [float(x) for x in ll[0]] if record_likelihood else None
     return FcaRun(params=FcaParams(S=S, v=v), stats=stats, counters=counters, loglik=hist)
 

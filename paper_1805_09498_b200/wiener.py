@@ -36,13 +36,10 @@ def mmse_images_fca(params: fca.FcaParams, obs: ObservationTensor) -> SeparatedI
 def mmse_images_fastfca(params: fastfca.FastFcaParams, stats: fastfca.TransformedStats) -> SeparatedImages:
     """Wiener estimates x_j = P^{-H} mu_tilde_j.  wiener.py:38-43.
 
-    When ``stats`` is the lazy refresh returned by ``run_fastfca`` for these
-    params, the device computes the images straight from (y, P, Lambda, v)
-    in one pass (mu_tilde is never materialised).
+    One device pass: P^{-H} per bin, then the back-solve written straight in
+    the (J, I, N, F) image layout.  (``fastfca.images_from_state`` fuses the
+    refresh too, for callers that never need mu_tilde.)
     """
-    src = getattr(stats, "_source", None)
-    if src is not None and stats._mu is None and src[1] is params:
-        return SeparatedImages(stft=fastfca.images_from_state(src[0], params))
     return SeparatedImages(stft=fastfca.back_transform_means(params.P, stats.mu, images_layout=True))
 
 

@@ -96,6 +96,27 @@ def make(cfg: Config, seed0: int = 0, mixtures: int | None = None):
     return y, P, lam, v
 
 
+def make_torch_range(cfg: Config, seed0: int, u0: int, u1: int, device):
+    """Mixtures u0..u1-1 of a config, mixture u drawn from its own torch generator (seed0 + u).
+
+    Every mixture depends only on its index, so shards of the mixture axis generated on
+    different ranks (bench.py --gpus N) are exactly the corresponding slices of the
+    single-GPU batch.  Same recipe and layouts as ``make_torch``.
+    """
+    import torch
+
+    parts = [make_torch(cfg, seed0 + u, 1, device) for u in range(u0, u1)]
+    if not parts:
+        cdt = torch.complex64 if cfg.dtype == "c64" else torch.complex128
+        rdt = torch.float32 if cfg.dtype == "c64" else torch.float64
+        I, J, F, N = cfg.I, cfg.J, cfg.F, cfg.N
+        return (torch.empty((0, I, N, F), dtype=cdt, device=device), torch.empty((0, F, I, I), dtype=cdt, device=device),
+                torch.empty((0, J, F, I), dtype=rdt, device=device), torch.empty((0, J, N, F), dtype=rdt, device=device))
+    out = tuple(torch.cat([p[k] for p in parts]) for k in range(4))
+    del parts
+    return out
+
+
 def make_torch(cfg: Config, seed: int, mixtures: int, device, chunk: int = 32):
     """The same recipe drawn with torch on the GPU (fast for the 256-mixture config).
 

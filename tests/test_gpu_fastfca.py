@@ -404,16 +404,59 @@ def test_partition_identity_images():
     # sum_j x_j = y (test_wiener.py:56-74; acceptance criterion 8)
     y, P0, lam0, v0, _ = mixture(12, 3, 3, 16, 40)
     run = fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=5)
-    fused = wiener.mmse_images_fastfca(run.params, run.stats).stft
+    fused = fastfca.images_from_state(ObservationTensor(y), run.params)
     assert np.abs(fused.sum(axis=0) - y).max() <= 1e-8 * np.abs(y).max()
-    explicit = wiener.mmse_images_fastfca(run.params, fastfca.TransformedStats(run.stats.mu, run.stats.phi)).stft
+    explicit = wiener.mmse_images_fastfca(run.params, run.stats).stft
+    assert np.abs(explicit.sum(axis=0) - y).max() <= 1e-8 * np.abs(y).max()
     assert rel(fused, explicit) <= 1e-12
+
+
+def test_stats_are_a_snapshot_of_the_final_state():
+    # the reference refreshes the statistics eagerly (fastfca.py:466): changing run.params
+    # afterwards must not change run.stats; the stats types are dataclasses (fastfca.py:87-96)
+    import dataclasses
+    y, P0, lam0, v0, _ = mixture(13, 3, 3, 8, 30)
+    run = fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=3)
+    ref = ffr.run_fastfca(y, P0, lam0, v0, iterations=3)
+    mu0 = run.stats.mu.copy()
+    run.params.P[...] = 0.0
+    run.params.v *= 2.0
+    assert np.array_equal(run.stats.mu, mu0)
+    assert rel(run.stats.mu, ref.mu) <= 1e-10 and rel(run.stats.phi, ref.phi) <= 1e-10
+    st = dataclasses.replace(run.stats, phi=None)
+    assert st.phi is None and set(dataclasses.asdict(run.stats)) == {"mu", "phi"}
+
+
+def test_batch_stats_match_single_runs():
+    y, P0, lam0, v0 = _stack(range(530, 533), 3, 3, 10, 45)
+    P, lam, v, ll, mu, phi = fastfca.run_fastfca_batch(y, P0, lam0, v0, iterations=4, stats=True)
+    for u in range(3):
+        run = fastfca.run_fastfca(ObservationTensor(y[u]), fastfca.FastFcaParams(P0[u], lam0[u], v0[u]),
+                                  iterations=4)
+        assert np.array_equal(run.stats.mu, mu[u]) and np.array_equal(run.stats.phi, phi[u])
+    os.environ["FFCA_PIPELINE_MIN_BYTES"] = "1"  # chunked host pipeline with the stats outputs
+    try:
+        got = fastfca.run_fastfca_batch(y, P0, lam0, v0, iterations=4, stats=True)
+    finally:
+        os.environ.pop("FFCA_PIPELINE_MIN_BYTES")
+    assert np.array_equal(got[4], mu) and np.array_equal(got[5], phi) and np.array_equal(got[2], v)
+    one = fastfca.run_fastfca_batch(y[:1], P0[:1], lam0[:1], v0[:1], iterations=4, stats=True)
+    os.environ["FFCA_PIPELINE_MIN_BYTES"] = "1"  # one mixture: frequency-block chunks
+    try:
+        blk = fastfca.run_fastfca_batch(y[:1], P0[:1], lam0[:1], v0[:1], iterations=4, stats=True)
+    finally:
+        os.environ.pop("FFCA_PIPELINE_MIN_BYTES")
+    for a, b in zip(blk, one):
+        if a is not None:
+            assert np.array_equal(a, b)
 
 
 def test_launch_count_is_one_kernel():
     y, P0, lam0, v0, _ = mixture(12, 3, 3, 16, 40)
+    fastfca.run_fastfca_batch(y[None], P0[None], lam0[None], v0[None], iterations=20)
+    assert _lib.launches() == 1  # the whole 20-iteration loop
     fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=20)
-    assert _lib.launches() == 1
+    assert _lib.launches() == 2  # + the final statistics refresh (fastfca.py:466)
 
 
 @pytest.mark.parametrize("shape", [(5, 3, 3, 40, 70), (1, 4, 4, 37, 300)])
@@ -547,3 +590,62 @@ def test_sharded_driver_device_path_world1():
             assert np.array_equal(P, Pr) and np.array_equal(v, vr) and np.allclose(ll, llr, rtol=1e-14)
     finally:
         dist.destroy_process_group()
+
+
+def _stack(seeds, I, J, F, N, rank=4):
+    parts = [mixture(s, I, J, F, N, rank) for s in seeds]
+    return tuple(np.stack([p[k] for p in parts]) for k in range(4))
+
+
+def _plan(dt_code, U, I, J, N, F):
+    out = np.zeros(6, np.int32)
+    _lib.load().ffca_plan_loop(0, dt_code, U, I, J, N, F, _lib.VF_AUTO, out.ctypes.data_as(_lib._ip))
+    return out
+
+
+def test_c128_results_do_not_depend_on_batch_size():
+    # config-0 shape, complex128: a lone mixture (513 bins, under one wave of 2-bin CTAs) runs
+    # one-bin CTAs, a batch of 4 runs 2-bin CTAs; the one-bin plan reduces over 16-lane
+    # segments so both give bitwise the same bins (the plans used to differ)
+    cfg = CONFIGS[0]
+    args = _stack(range(500, 504), cfg.I, cfg.J, cfg.F, cfg.N)
+    assert _plan(_lib.C128, 1, 3, 3, cfg.N, cfg.F)[0] == 1
+    assert _plan(_lib.C128, 4, 3, 3, cfg.N, cfg.F)[0] == 2
+    os.environ["FFCA_NO_PIPELINE"] = "1"
+    try:
+        batch = fastfca.run_fastfca_batch(*args, iterations=5, record_likelihood=True)
+        for u in (0, 3):
+            one = fastfca.run_fastfca_batch(*(a[u:u + 1] for a in args), iterations=5, record_likelihood=True)
+            for a, b in zip(one, batch):
+                assert np.array_equal(a[0], b[u])
+    finally:
+        os.environ.pop("FFCA_NO_PIPELINE")
+
+
+def test_c128_pipelined_chunks_bitwise_one_launch():
+    # 3 config-0 mixtures (69 MB) take the host pipeline in chunks of 2 + 1 mixtures; the 1-mixture
+    # chunk runs the one-bin plan while one launch of all 3 runs 2-bin CTAs
+    cfg = CONFIGS[0]
+    args = _stack(range(510, 513), cfg.I, cfg.J, cfg.F, cfg.N)
+    os.environ["FFCA_NO_PIPELINE"] = "1"
+    try:
+        ref = fastfca.run_fastfca_batch(*args, iterations=4, record_likelihood=True)
+    finally:
+        os.environ.pop("FFCA_NO_PIPELINE")
+    got = fastfca.run_fastfca_batch(*args, iterations=4, record_likelihood=True)
+    for a, b in zip(got, ref):
+        assert np.array_equal(a, b)
+
+
+def test_batch_coerces_mixed_precision_inputs():
+    # complex128 y with complex64 / float32 state: the state is promoted to y's precision, and
+    # the result equals the all-complex128 call (no host-buffer overrun)
+    y, P0, lam0, v0 = _stack(range(520, 522), 3, 3, 9, 40)
+    ref = fastfca.run_fastfca_batch(y, P0, lam0, v0, iterations=3)
+    got = fastfca.run_fastfca_batch(y, P0.astype(np.complex64), lam0.astype(np.float32),
+                                    v0.astype(np.float32), iterations=3)
+    assert got[0].dtype == np.complex128 and got[2].dtype == np.float64
+    ref32 = fastfca.run_fastfca_batch(y, P0, lam0, v0.astype(np.float32).astype(np.float64), iterations=3)
+    for a, b in zip(got[:3], ref32[:3]):
+        assert np.array_equal(a, b)
+    assert rel(got[0], ref[0]) <= 1e-4

@@ -121,3 +121,21 @@ def test_eval_report_rows_and_summary():
     row = r.row()
     assert row["sdr_mean"] == "6.000000" and row["sdr_2"] == "7.000000" and row["inversions"] == 40960
     assert row["rtf_ratio_measured"] == "1.3" and "fastfca: I=3 J=3" in r.summary()
+
+
+def test_batch_entry_validates_before_the_abi():
+    # run_fastfca_batch checks dtypes / shapes / out buffers on the host before any C-ABI call
+    y = np.ones((2, 3, 5, 4), np.complex128)
+    P0 = np.broadcast_to(np.eye(3), (2, 4, 3, 3)).astype(np.complex64)
+    lam0 = np.ones((2, 2, 4, 3), np.float32)
+    v0 = np.ones((2, 2, 5, 4), np.float32)
+    with pytest.raises(errors.DimensionMismatch):
+        fastfca.run_fastfca_batch(np.ones((2, 3, 5, 4)), P0, lam0, v0)  # real y
+    with pytest.raises(errors.DimensionMismatch):
+        fastfca.run_fastfca_batch(y, P0[:, :3], lam0, v0)
+    bad_out = (np.empty((2, 4, 3, 3), np.complex64), np.empty((2, 2, 4, 3)), np.empty((2, 2, 5, 4)))
+    with pytest.raises(ValueError):  # complex128 y -> complex128 P out expected
+        fastfca.run_fastfca_batch(y, P0, lam0, v0, out=bad_out)
+    short = (np.empty((2, 4, 3, 3), np.complex128), np.empty((2, 2, 4, 3)), np.empty((1, 2, 5, 4)))
+    with pytest.raises(ValueError):
+        fastfca.run_fastfca_batch(y, P0, lam0, v0, out=short)
