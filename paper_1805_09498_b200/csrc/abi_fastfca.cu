@@ -250,6 +250,7 @@ static int launch_problem(int device, const DevProblem& d, cudaStream_t s) {
     pa.RS = loop_rs(d.I, JM);
     pa.JS = loop_js(d.I, JM, d.J);
     pa.ilv = loop_interleaved(d.I) ? 1 : 0;
+    pa.pairs = loop_pairs(d.I, int(rsize(d.dtype))) ? 1 : 0;
     pa.total_bins = nb;
     pa.ngroups = (nb + p.G - 1) / p.G;
     pa.slab_bytes = (long long)p.slab;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cooperative_groups.h>
 #include <cstdint>
+#include <type_traits>
 
 namespace ffca {
 
@@ -87,6 +88,16 @@ __device__ __forceinline__ float2 upk64(unsigned long long r) {
 __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
   unsigned long long r;
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk64(a)), "l"(pk64(b)), "l"(pk64(c)));
+  return upk64(r);
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk64(a)), "l"(pk64(b)));
+  return upk64(r);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk64(a)), "l"(pk64(b)));
   return upk64(r);
 }
 __device__ __forceinline__ double2 fma2(double2 a, double2 b, double2 c) {
@@ -321,6 +332,70 @@ struct SmallLDL {
         x[r].x -= lv.x * x[c].x + lv.y * x[c].y;
         x[r].y -= lv.x * x[c].y - lv.y * x[c].x;
       }
+  }
+};
+
+// Hermitian I x I (I <= 3) inverse applied through the adjugate: B^-1 = adj(B) / det(B).  Same
+// interface as SmallLDL (factor: B's lower triangle, diagonal real; ok = det(B) != 0, the exact
+// singularity the reference's LU inverse rejects; solve: x <- B^-1 x).  Every cofactor is an
+// independent 2 x 2 determinant, so the dependency chain is a few operations deep instead of the
+// factorisation's pivot-by-pivot chain (the solve is on every iteration's critical path).
+template <int I>
+struct HermAdj {
+  static_assert(I >= 1 && I <= 3, "adjugate solve for I <= 3");
+  double a[I];        // real diagonal of adj(B)
+  double2 c[I][I];    // lower triangle of adj(B) (c[r][q], q < r); upper = conj
+  double rdet;        // 1 / det(B)
+  bool ok;
+
+  __device__ __forceinline__ void factor(const double2 (&b)[I][I]) {
+    double det;
+    if constexpr (I == 1) {
+      a[0] = 1.0;
+      det = b[0][0].x;
+    } else if constexpr (I == 2) {
+      a[0] = b[1][1].x;
+      a[1] = b[0][0].x;
+      c[1][0] = make_double2(-b[1][0].x, -b[1][0].y);
+      det = b[0][0].x * b[1][1].x - (b[1][0].x * b[1][0].x + b[1][0].y * b[1][0].y);
+    } else {
+      const double b00 = b[0][0].x, b11 = b[1][1].x, b22 = b[2][2].x;
+      const double2 b10 = b[1][0], b20 = b[2][0], b21 = b[2][1];
+      a[0] = b11 * b22 - (b21.x * b21.x + b21.y * b21.y);
+      a[1] = b00 * b22 - (b20.x * b20.x + b20.y * b20.y);
+      a[2] = b00 * b11 - (b10.x * b10.x + b10.y * b10.y);
+      // (B^-1)_10 ~ -(b10 b22 - conj(b21) b20)
+      c[1][0] = make_double2(-(b10.x * b22 - (b21.x * b20.x + b21.y * b20.y)),
+                             -(b10.y * b22 - (b21.x * b20.y - b21.y * b20.x)));
+      // (B^-1)_20 ~ b10 b21 - b11 b20
+      c[2][0] = make_double2(b10.x * b21.x - b10.y * b21.y - b11 * b20.x, b10.x * b21.y + b10.y * b21.x - b11 * b20.y);
+      // (B^-1)_21 ~ -(b00 b21 - conj(b10) b20)
+      c[2][1] = make_double2(-(b00 * b21.x - (b10.x * b20.x + b10.y * b20.y)),
+                             -(b00 * b21.y - (b10.x * b20.y - b10.y * b20.x)));
+      // det = b00 a0 + 2 Re(conj(b10) c10 ... ) written via the first column of adj
+      det = b00 * a[0] + (b10.x * c[1][0].x + b10.y * c[1][0].y) + (b20.x * c[2][0].x + b20.y * c[2][0].y);
+    }
+    ok = det != 0.0;
+    rdet = ok ? rcp(det) : 0.0;
+  }
+
+  __device__ __forceinline__ void solve(double2 (&x)[I]) const {
+    double2 y[I];
+#pragma unroll
+    for (int r = 0; r < I; ++r) {
+      double2 acc = make_double2(a[r] * x[r].x, a[r] * x[r].y);
+#pragma unroll
+      for (int q = 0; q < I; ++q) {
+        if (q == r) continue;
+        // adj[r][q] = c[r][q] (q < r) or conj(c[q][r]) (q > r)
+        const double2 m = q < r ? c[r][q] : make_double2(c[q][r].x, -c[q][r].y);
+        acc.x += m.x * x[q].x - m.y * x[q].y;
+        acc.y += m.x * x[q].y + m.y * x[q].x;
+      }
+      y[r] = acc;
+    }
+#pragma unroll
+    for (int r = 0; r < I; ++r) x[r] = make_double2(y[r].x * rdet, y[r].y * rdet);
   }
 };
 

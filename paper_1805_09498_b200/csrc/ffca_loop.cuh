@@ -72,6 +72,22 @@ __host__ __device__ constexpr int loop_js(int I, int JM, int J) { return loop_in
 // I > 4 solve: the 8-lane group that inverts P is the first group of the warp after the I
 // groups of the B_i (so it never shares a warp with them); the CTA needs 8 (mP + 1) threads.
 __host__ __device__ constexpr int loop_pgroup(int I) { return (I + 3) / 4 * 4; }
+// complex64, I <= 4: frame-pair records.  Frames 2m and 2m + 1 of a bin share one record (twice the
+// per-frame record): channel i's two observations are adjacent (one 16-byte load gives y_i of both
+// frames) and the powers are stored as (v_j(2m), v_j(2m + 1)) pairs, so the per-point arithmetic
+// runs on packed frame pairs (FFMA2) -- weights, reciprocals, the v update and the sums over frames
+// all operate on both frames at once.  Strides stay odd multiples of 16 / 8 bytes: conflict free.
+__host__ __device__ constexpr bool loop_pairs(int I, int rsz) { return !loop_interleaved(I) && rsz == 4; }
+// Slab element offsets of frame n, bin g: y channel i in complex units, v source j in reals
+// (RS complex / JS reals per frame record).
+template <bool PAIRS>
+__host__ __device__ __forceinline__ int slab_y(int n, int g, int i, int G, int RS) {
+  return PAIRS ? ((n >> 1) * G + g) * 2 * RS + 2 * i + (n & 1) : (n * G + g) * RS + i;
+}
+template <bool PAIRS>
+__host__ __device__ __forceinline__ int slab_v(int n, int g, int j, int G, int JS) {
+  return PAIRS ? ((n >> 1) * G + g) * 2 * JS + 2 * j + (n & 1) : (n * G + g) * JS + j;
+}
 
 template <int I, int JM>
 struct Shape {
@@ -110,9 +126,10 @@ struct LoopSmem {
     const size_t csz = 2 * size_t(rsz);
     const bool ilv = loop_interleaved(I);
     const int JS = loop_js(I, JM, J);
-    ybytes = align16(size_t(NL) * G * loop_rs(I, JM) * csz);
-    vbytes = ilv ? 0 : align16(size_t(NL) * G * JS * rsz);
-    const size_t fs = vf_mode == 2 ? align16(size_t(NL) * G * JS * rsz) : 0;
+    const size_t NLs = loop_pairs(I, rsz) ? size_t((NL + 1) & ~1) : size_t(NL);  // frame-pair records
+    ybytes = align16(NLs * G * loop_rs(I, JM) * csz);
+    vbytes = ilv ? 0 : align16(NLs * G * JS * rsz);
+    const size_t fs = vf_mode == 2 ? align16(NLs * G * JS * rsz) : 0;
     slab = ybytes + vbytes + fs;
     if (resident) {
       y = o; o += ybytes;
@@ -265,7 +282,11 @@ __device__ __forceinline__ void bin_reduce(const R (&vals)[V], T* wpart, double*
 #pragma unroll
   for (int k = 0; k < V2; ++k) buf[k] = k < V ? vals[k] : R(0);
   int base = 0;
+#ifdef FFCA_EXP_SKIP_BUTTERFLY  // timing experiment only: no cross-lane sums (results are wrong)
+  base = (lane / G) % L * (V2 / L);
+#else
   halving_step<R, V2, G * SEG / 2, G>(buf, lane, base);
+#endif
   const int vw = warp * NSEG + lane / (G * SEG);  // (virtual) warp row in slot order
   T* row = wpart + (vw * G + g) * VMAX;  // warp partials (the loop kernel keeps them in its compute type)
 #pragma unroll
@@ -338,6 +359,7 @@ template <typename R, int I, int JM, int G>
 struct PointWork {
   using C2 = typename Cpx<R>::T;
   static constexpr int IC = Shape<I, JM>::IC, NB = Shape<I, JM>::NB, RS = Shape<I, JM>::RS;
+  static constexpr int NCXP = I * (I - 1) / 2 > 0 ? I * (I - 1) / 2 : 1;  // complex off-diagonal entries
   static constexpr bool PREG = Shape<I, JM>::PREG;
   static constexpr int VA = JM * (1 + I) + 1;
 
@@ -351,8 +373,12 @@ struct PointWork {
   R wfl, invI;
   static constexpr int IP2 = (I + 1) / 2;  // lambda stored as (i, i+1) pairs for FFMA2
   static constexpr int PFD = 2;            // prefetch distance (frames of this thread) on a global slab
+  static constexpr bool PAIRS = loop_pairs(I, int(sizeof(R)));  // frame-pair records (complex64, I <= 4)
   C2 Pr[PREG ? I : 1][PREG ? I : 1];
-  C2 Lp[PREG ? JM : 1][PREG ? IP2 : 1];
+  C2 Lp[PREG && !PAIRS ? JM : 1][PREG && !PAIRS ? IP2 : 1];  // lambda as (i, i+1) pairs (FFMA2 over i)
+  R Ls[PAIRS ? JM : 1][PAIRS ? I : 1];                        // PAIRS: lambda as scalars (broadcast operands)
+  int nfull;  // PAIRS: full frame pairs of this thread
+  bool part;  // PAIRS: this thread also owns the bin's last, half-filled pair (odd frame count)
 
   __device__ __forceinline__ void load_PL() {
     if constexpr (PREG) {
@@ -360,14 +386,21 @@ struct PointWork {
       for (int x = 0; x < I; ++x)
 #pragma unroll
         for (int y2 = 0; y2 < I; ++y2) Pr[x][y2] = Pc[(g * I + x) * I + y2];
+      if constexpr (PAIRS) {
 #pragma unroll
-      for (int j = 0; j < JM; ++j)
+        for (int j = 0; j < JM; ++j)
 #pragma unroll
-        for (int ip = 0; ip < IP2; ++ip) {
-          const R l0 = (j < J) ? lamc[(g * J + j) * I + 2 * ip] : R(0);
-          const R l1 = (j < J && 2 * ip + 1 < I) ? lamc[(g * J + j) * I + 2 * ip + 1] : R(0);
-          Lp[j][ip] = mk<C2, R>(l0, l1);
-        }
+          for (int i = 0; i < I; ++i) Ls[j][i] = (j < J) ? lamc[(g * J + j) * I + i] : R(0);
+      } else {
+#pragma unroll
+        for (int j = 0; j < JM; ++j)
+#pragma unroll
+          for (int ip = 0; ip < IP2; ++ip) {
+            const R l0 = (j < J) ? lamc[(g * J + j) * I + 2 * ip] : R(0);
+            const R l1 = (j < J && 2 * ip + 1 < I) ? lamc[(g * J + j) * I + 2 * ip + 1] : R(0);
+            Lp[j][ip] = mk<C2, R>(l0, l1);
+          }
+      }
     }
   }
   __device__ __forceinline__ C2 P(int x, int y2) const {
@@ -375,7 +408,8 @@ struct PointWork {
     else return Pc[(g * I + x) * I + y2];
   }
   __device__ __forceinline__ R Lam(int j, int i) const {
-    if constexpr (PREG) return (i & 1) ? Lp[j][i >> 1].y : Lp[j][i >> 1].x;
+    if constexpr (PAIRS) return Ls[j][i];
+    else if constexpr (PREG) return (i & 1) ? Lp[j][i >> 1].y : Lp[j][i >> 1].x;
     else return lamc[(g * J + j) * I + i];
   }
   // y_t = P^H y ; q = |y_t|^2   (fastfca.py:442-446)
@@ -791,6 +825,217 @@ struct PointWork {
     }
   }
 
+  // ---------------- frame-pair point work (PAIRS: complex64, I <= 4) ----------------
+  // One record holds frames a = 2m and b = 2m + 1.  Quantities of one point are frame pairs
+  // (x = frame a, y = frame b), so every scalar step of the per-point algebra of phaseA / phaseB
+  // becomes one packed FFMA2 for both frames; sums over frames are kept as (even, odd) pairs and
+  // added at the end.  PART: frame b is the zero padding after an odd frame count -- its power
+  // stays 0 and it contributes nothing (its floor is replaced by 1 so 0 / v' is 0, never 0 / 0).
+  __device__ __forceinline__ void load_pair(const C2* yp, const R* vp, C2 (&ya)[I], C2 (&yb)[I], C2 (&v2)[JM]) const {
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      const float4 t = *(const float4*)(yp + 2 * i);
+      ya[i] = mk<C2, R>(t.x, t.y);
+      yb[i] = mk<C2, R>(t.z, t.w);
+    }
+#pragma unroll
+    for (int j = 0; j < JM; ++j) v2[j] = (j < J) ? *(const C2*)(vp + 2 * j) : mk<C2, R>(R(0), R(0));
+  }
+  // q_b = |(P^H y)_b|^2 for both frames, as a pair
+  __device__ __forceinline__ void q_pair(const C2 (&ya)[I], const C2 (&yb)[I], C2 (&q2)[I]) const {
+#pragma unroll
+    for (int b = 0; b < I; ++b) {
+      C2 ta = mk<C2, R>(R(0), R(0)), tb = ta;
+#pragma unroll
+      for (int x = 0; x < I; ++x) {
+        const C2 pp = P(x, b);
+        ta = fma2(ya[x], bc2<R>(pp.x), ta);
+        ta = fma2(mk<C2, R>(ya[x].y, -ya[x].x), bc2<R>(pp.y), ta);
+        tb = fma2(yb[x], bc2<R>(pp.x), tb);
+        tb = fma2(mk<C2, R>(yb[x].y, -yb[x].x), bc2<R>(pp.y), tb);
+      }
+      q2[b] = mk<C2, R>(ta.x * ta.x + ta.y * ta.y, tb.x * tb.x + tb.y * tb.y);
+    }
+  }
+  // floored weights w_i = max(sum_j v_j lambda_ji, floor) of both frames; returns 1 / w
+  __device__ __forceinline__ void iw_pair(const C2 (&v2)[JM], C2 (&iw2)[I], C2 (&w2)[I]) const {
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      C2 w = mk<C2, R>(R(0), R(0));
+#pragma unroll
+      for (int j = 0; j < JM; ++j)
+        if (j < J) w = fma2(v2[j], bc2<R>(Lam(j, i)), w);
+      w = mk<C2, R>(fmax(w.x, wfl), fmax(w.y, wfl));
+      w2[i] = w;
+      iw2[i] = mk<C2, R>(rcp_pt(w.x), rcp_pt(w.y));
+    }
+  }
+
+  template <bool REC, bool VF2, bool PART>
+  __device__ __forceinline__ void pairA(const C2* yp, R* vp, const R* fp, C2 (&s0)[JM], C2 (&s1)[JM][I], C2& lacc,
+                                        const R vfl_b) const {
+    C2 ya[I], yb[I], v2[JM];
+    load_pair(yp, vp, ya, yb, v2);
+    C2 q2[I], iw2[I], w2[I], d2[I];
+    q_pair(ya, yb, q2);
+    iw_pair(v2, iw2, w2);
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      d2[i] = mul2(fma2(q2[i], iw2[i], bc2<R>(R(-1))), iw2[i]);  // d = q / w^2 - 1 / w
+      if constexpr (REC)
+        lacc = add2(lacc, mk<C2, R>(flog(w2[i].x) + q2[i].x * iw2[i].x,
+                                    PART ? R(0) : flog(w2[i].y) + q2[i].y * iw2[i].y));
+    }
+#pragma unroll
+    for (int j = 0; j < JM; ++j) {
+      if (j < J) {
+        C2 sd = mk<C2, R>(R(0), R(0));  // r2 - r1
+#pragma unroll
+        for (int i = 0; i < I; ++i) sd = fma2(bc2<R>(Lam(j, i)), d2[i], sd);
+        C2 fl = bc2<R>(vfl_b);
+        if constexpr (VF2) fl = *(const C2*)(fp + 2 * j);
+        // v' = max(v - v^2 (r1 - r2) / I, floor)   (fastfca.py:336-337)
+        C2 vn = fma2(sd, mul2(mul2(v2[j], v2[j]), bc2<R>(invI)), v2[j]);
+        vn = mk<C2, R>(fmax(vn.x, fl.x), fmax(vn.y, fl.y));
+        if constexpr (PART) {
+          *(C2*)(vp + 2 * j) = mk<C2, R>(vn.x, R(0));  // the padding frame keeps v = 0
+          vn.y = R(1);
+        } else {
+          *(C2*)(vp + 2 * j) = vn;
+        }
+        const C2 ratio = mul2(v2[j], mk<C2, R>(rcp_pt(vn.x), rcp_pt(vn.y)));
+        s0[j] = add2(s0[j], ratio);
+        const C2 rv = mul2(ratio, v2[j]);
+#pragma unroll
+        for (int i = 0; i < I; ++i) s1[j][i] = fma2(rv, d2[i], s1[j][i]);
+      }
+    }
+  }
+
+  template <bool REC, bool VF2>
+  __device__ __forceinline__ void phaseA_pairs(R (&acc)[VA], const R vfl_b) const {
+    C2 s0[JM], s1[JM][I], lacc = mk<C2, R>(R(0), R(0));
+#pragma unroll
+    for (int j = 0; j < JM; ++j) {
+      s0[j] = lacc;
+#pragma unroll
+      for (int i = 0; i < I; ++i) s1[j][i] = lacc;
+    }
+    const C2* yp = ys + rec0 * 2 * RS;
+    R* vp = vs + rec0 * 2 * JS;
+    const R* fp = vfs + rec0 * 2 * JS;
+    const int sy = rstep * 2 * RS, sv = rstep * 2 * JS;
+#pragma unroll 1
+    for (int k = 0; k < nfull; ++k, yp += sy, vp += sv, fp += sv) pairA<REC, VF2, false>(yp, vp, fp, s0, s1, lacc, vfl_b);
+    if (part) pairA<REC, VF2, true>(yp, vp, fp, s0, s1, lacc, vfl_b);
+#pragma unroll
+    for (int j = 0; j < JM; ++j) {
+      acc[j] = s0[j].x + s0[j].y;
+#pragma unroll
+      for (int i = 0; i < I; ++i) acc[JM + j * I + i] = s1[j][i].x + s1[j][i].y;
+    }
+    acc[VA - 1] = lacc.x + lacc.y;
+  }
+
+  template <bool REC, bool PART>
+  __device__ __forceinline__ void pairB(const C2* yp, const R* vp, C2 (&ac)[I][NCXP], C2 (&ad)[I][I], C2& lacc) const {
+    C2 ya[I], yb[I], v2[JM];
+    load_pair(yp, vp, ya, yb, v2);
+    C2 iw2[I], w2[I];
+    iw_pair(v2, iw2, w2);
+    if constexpr (REC) {
+      C2 q2[I];
+      q_pair(ya, yb, q2);
+#pragma unroll
+      for (int i = 0; i < I; ++i)
+        lacc = add2(lacc, mk<C2, R>(flog(w2[i].x) + q2[i].x * iw2[i].x,
+                                    PART ? R(0) : flog(w2[i].y) + q2[i].y * iw2[i].y));
+    }
+    C2 dg[I];
+#pragma unroll
+    for (int x = 0; x < I; ++x)
+      dg[x] = mk<C2, R>(ya[x].x * ya[x].x + ya[x].y * ya[x].y, yb[x].x * yb[x].x + yb[x].y * yb[x].y);
+    C2 za[NCXP], zb[NCXP];
+    {
+      int c = 0;
+#pragma unroll
+      for (int x = 1; x < I; ++x)
+#pragma unroll
+        for (int y2 = 0; y2 < x; ++y2, ++c) {  // y_x conj(y_y) = y_y.x (y_x) + y_y.y (y_x.y, -y_x.x)
+          za[c] = fma2(mk<C2, R>(ya[x].y, -ya[x].x), bc2<R>(ya[y2].y), fma2(ya[x], bc2<R>(ya[y2].x), mk<C2, R>(R(0), R(0))));
+          zb[c] = fma2(mk<C2, R>(yb[x].y, -yb[x].x), bc2<R>(yb[y2].y), fma2(yb[x], bc2<R>(yb[y2].x), mk<C2, R>(R(0), R(0))));
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+#pragma unroll
+      for (int c = 0; c < NCXP; ++c) {
+        if (c < I * (I - 1) / 2) {
+          ac[i][c] = fma2(za[c], bc2<R>(iw2[i].x), ac[i][c]);
+          ac[i][c] = fma2(zb[c], bc2<R>(iw2[i].y), ac[i][c]);
+        }
+      }
+#pragma unroll
+      for (int x = 0; x < I; ++x) ad[i][x] = fma2(dg[x], iw2[i], ad[i][x]);
+    }
+  }
+
+  // Phase B on frame pairs: B_i = sum_n y y^H / w_i (fastfca.py:352-358), packed lower triangle.
+  template <bool REC>
+  __device__ __forceinline__ void phaseB_pairs(R (&acc)[NB + 1]) const {
+    C2 ac[I][NCXP], ad[I][I], lacc = mk<C2, R>(R(0), R(0));
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+#pragma unroll
+      for (int c = 0; c < NCXP; ++c) ac[i][c] = lacc;
+#pragma unroll
+      for (int x = 0; x < I; ++x) ad[i][x] = lacc;
+    }
+    const C2* yp = ys + rec0 * 2 * RS;
+    const R* vp = vs + rec0 * 2 * JS;
+    const int sy = rstep * 2 * RS, sv = rstep * 2 * JS;
+#pragma unroll 1
+    for (int k = 0; k < nfull; ++k, yp += sy, vp += sv) pairB<REC, false>(yp, vp, ac, ad, lacc);
+    if (part) pairB<REC, true>(yp, vp, ac, ad, lacc);
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      R* o = acc + i * I * I;
+      int c = 0;
+#pragma unroll
+      for (int x = 0; x < I; ++x) {
+        o[x * x] = ad[i][x].x + ad[i][x].y;
+#pragma unroll
+        for (int y2 = 0; y2 < x; ++y2, ++c) {
+          o[x * x + 1 + 2 * y2] = ac[i][c].x;
+          o[x * x + 2 + 2 * y2] = ac[i][c].y;
+        }
+      }
+    }
+    acc[NB] = lacc.x + lacc.y;
+  }
+
+  // Likelihood partial on frame pairs (after the last P update).
+  __device__ __forceinline__ void phaseL_pairs(R (&acc)[1]) const {
+    C2 lacc = mk<C2, R>(R(0), R(0));
+    const C2* yp = ys + rec0 * 2 * RS;
+    const R* vp = vs + rec0 * 2 * JS;
+    const int sy = rstep * 2 * RS, sv = rstep * 2 * JS;
+    const int n = nfull + (part ? 1 : 0);
+#pragma unroll 1
+    for (int k = 0; k < n; ++k, yp += sy, vp += sv) {
+      const bool half = part && k == n - 1;
+      C2 ya[I], yb[I], v2[JM], q2[I], iw2[I], w2[I];
+      load_pair(yp, vp, ya, yb, v2);
+      q_pair(ya, yb, q2);
+      iw_pair(v2, iw2, w2);
+#pragma unroll
+      for (int i = 0; i < I; ++i)
+        lacc = add2(lacc, mk<C2, R>(flog(w2[i].x) + q2[i].x * iw2[i].x,
+                                    half ? R(0) : flog(w2[i].y) + q2[i].y * iw2[i].y));
+    }
+    acc[0] += lacc.x + lacc.y;
+  }
+
   // Likelihood partial sum_n,i ln w + q / w at the current state.
   __device__ __forceinline__ void phaseL(R (&acc)[1]) const {
     const C2* yp = ys + rec0 * RS;
@@ -842,6 +1087,7 @@ struct PackArgs {
   void* packed;
   int I, J, N, F, G, C, RS, JS, FT;
   int ilv;
+  int pairs;  // frame-pair records (loop_pairs)
   long long total_bins, ngroups, slab_bytes;
   long long Ly, Lv;  // record regions inside an image
 };
@@ -891,8 +1137,8 @@ __global__ void __launch_bounds__(256) slab_pack_kernel(const PackArgs a) {
     const long long q = b0 / G + qi;
     if (q >= a.ngroups) continue;
     unsigned char* img = (unsigned char*)a.packed + (q * C + rk[nt]) * a.slab_bytes;
-    const int rec = nlk[nt] * G + g;
-    C2* yr = (C2*)(img + a.Ly) + (long long)rec * RS;
+    const int nl = nlk[nt];
+    C2* yr = (C2*)(img + a.Ly);
     const C2* src = yt + (nt * 32 + col) * I;
     const R* vsrc = vt + (nt * 32 + col) * J;
     for (int s = 0; s < RS; ++s) {
@@ -903,11 +1149,12 @@ __global__ void __launch_bounds__(256) slab_pack_kernel(const PackArgs a) {
         const int j = 2 * (s - I);
         val = mk<C2, R>(j < J ? vsrc[j] : R(0), j + 1 < J ? vsrc[j + 1] : R(0));
       }
-      yr[s] = val;
+      yr[a.pairs ? slab_y<true>(nl, g, s, G, RS) : slab_y<false>(nl, g, s, G, RS)] = val;
     }
     if (!a.ilv) {
-      R* vr = (R*)(img + a.Lv) + (long long)rec * JS;
-      for (int j = 0; j < JS; ++j) vr[j] = j < J ? vsrc[j] : R(0);
+      R* vr = (R*)(img + a.Lv);
+      for (int j = 0; j < JS; ++j)
+        vr[a.pairs ? slab_v<true>(nl, g, j, G, JS) : slab_v<false>(nl, g, j, G, JS)] = j < J ? vsrc[j] : R(0);
     }
   }
 }
@@ -929,6 +1176,7 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
   const int slot = tid / G, nslots = blockDim.x / G;
   // complex128 one-bin CTAs reduce over 16-lane segments (bin_reduce): bitwise the G = 2 plan
   constexpr int SEG = (G == 1 && I <= 4 && sizeof(R) == 8) ? 16 : 32 / G;
+  constexpr bool PAIRS = loop_pairs(I, int(sizeof(R)));
 
   extern __shared__ __align__(16) unsigned char smem[];
   const int W = blockDim.x >> 5;
@@ -946,6 +1194,7 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
   const int n1 = int((long long)(crank + 1) * N / C);
   const int NLr = n1 - n0;
   const int NL = a.NL;
+  const int NLs = PAIRS ? (NL + 1) & ~1 : NL;  // frames the slab holds (frame pairs: even)
 
   unsigned char* slab = resident ? smem : (unsigned char*)a.scratch + (long long)blockIdx.x * a.slab_bytes;
   C2* ys = (C2*)(slab + L.y);
@@ -995,33 +1244,47 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
   if (!(a.packed && resident)) {
     const R* vfg = (const R*)a.vf;
     if (resident) {
+      // Pointer-bumped frame loops: iteration k copies frame slot + k * nslots (nslots is even, so
+      // the slab offset advances by a constant in both record layouts); frames >= NLr zero-fill.
+      const int nit = slot < NLs ? (NLs - slot + nslots - 1) / nslots : 0;
+      const int nok = (active && slot < NLr) ? (NLr - slot + nslots - 1) / nslots : 0;
+      const long long gstep = (long long)nslots * F;
+      const int ystep = nslots * G * RS, vstep = nslots * G * JS;
 #pragma unroll 1
-      for (int i = 0; i < I; ++i)
-        for (int n = slot; n < NL; n += nslots) {
-          const bool ok = active && n < NLr;
-          const C2* src = ok ? yg + ((u * I + i) * (long long)N + n0 + n) * F + f : yg;
-          cp_async<sizeof(C2)>(ys + (n * G + g) * RS + i, src, ok);
-        }
+      for (int i = 0; i < I; ++i) {
+        const C2* col = yg + ((u * I + i) * (long long)N + n0) * F + f;
+        const C2* src = col + (long long)slot * F;
+        C2* dst = ys + slab_y<PAIRS>(slot, g, i, G, RS);
 #pragma unroll 1
-      for (int j = 0; j < J; ++j)
-        for (int n = slot; n < NL; n += nslots) {
-          const bool ok = active && n < NLr;
-          const long long off = ((u * J + j) * (long long)N + n0 + n) * F + f;
-          cp_async<sizeof(R)>(vs + (n * G + g) * JS + j, ok ? vg + off : vg, ok);
-          if (a.vf_mode == 2) cp_async<sizeof(R)>(vfs + (n * G + g) * JS + j, ok ? vfg + off : vfg, ok);
+        for (int k = 0; k < nit; ++k, src += gstep, dst += ystep) cp_async<sizeof(C2)>(dst, k < nok ? src : col, k < nok);
+      }
+#pragma unroll 1
+      for (int j = 0; j < J; ++j) {
+        const long long c0 = ((u * J + j) * (long long)N + n0) * F + f;
+        const R* src = vg + c0 + (long long)slot * F;
+        R* dst = vs + slab_v<PAIRS>(slot, g, j, G, JS);
+#pragma unroll 1
+        for (int k = 0; k < nit; ++k, src += gstep, dst += vstep) cp_async<sizeof(R)>(dst, k < nok ? src : vg + c0, k < nok);
+        if (a.vf_mode == 2) {
+          const R* fsrc = vfg + c0 + (long long)slot * F;
+          R* fdst = vfs + slab_v<PAIRS>(slot, g, j, G, JS);
+#pragma unroll 1
+          for (int k = 0; k < nit; ++k, fsrc += gstep, fdst += vstep)
+            cp_async<sizeof(R)>(fdst, k < nok ? fsrc : vfg + c0, k < nok);
         }
+      }
     } else {
       for (int i = 0; i < I; ++i)
-        for (int n = slot; n < NL; n += nslots) {
+        for (int n = slot; n < NLs; n += nslots) {
           const bool ok = active && n < NLr;
-          ys[(n * G + g) * RS + i] = ok ? yg[((u * I + i) * (long long)N + n0 + n) * F + f] : mk<C2, R>(R(0), R(0));
+          ys[slab_y<PAIRS>(n, g, i, G, RS)] = ok ? yg[((u * I + i) * (long long)N + n0 + n) * F + f] : mk<C2, R>(R(0), R(0));
         }
       for (int j = 0; j < J; ++j)
-        for (int n = slot; n < NL; n += nslots) {
+        for (int n = slot; n < NLs; n += nslots) {
           const bool ok = active && n < NLr;
           const long long off = ((u * J + j) * (long long)N + n0 + n) * F + f;
-          vs[(n * G + g) * JS + j] = ok ? vg[off] : R(0);
-          if (a.vf_mode == 2) vfs[(n * G + g) * JS + j] = ok ? vfg[off] : R(0);
+          vs[slab_v<PAIRS>(n, g, j, G, JS)] = ok ? vg[off] : R(0);
+          if (a.vf_mode == 2) vfs[slab_v<PAIRS>(n, g, j, G, JS)] = ok ? vfg[off] : R(0);
         }
     }
   }
@@ -1050,10 +1313,16 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
   cp_async_wait_all();
   if (a.packed && resident) {
     mbar_wait(&gather_bar, 0);
-    if (NL > NLr) {  // frames past this CTA's range: zero records, as the element gather leaves them
-      for (int t = tid; t < (NL - NLr) * G * RS; t += blockDim.x) ys[NLr * G * RS + t] = mk<C2, R>(R(0), R(0));
+    if (NLs > NLr) {  // frames past this CTA's range: zero records, as the element gather leaves them
+      for (int t = tid; t < (NLs - NLr) * G * RS; t += blockDim.x) {
+        const int n = NLr + t / (G * RS), e = t % (G * RS);
+        ys[slab_y<PAIRS>(n, e / RS, e % RS, G, RS)] = mk<C2, R>(R(0), R(0));
+      }
       if (!Shape<I, JM>::ILV)
-        for (int t = tid; t < (NL - NLr) * G * JS; t += blockDim.x) vs[NLr * G * JS + t] = R(0);
+        for (int t = tid; t < (NLs - NLr) * G * JS; t += blockDim.x) {
+          const int n = NLr + t / (G * JS), e = t % (G * JS);
+          vs[slab_v<PAIRS>(n, e / JS, e % JS, G, JS)] = R(0);
+        }
     }
   }
   __syncthreads();
@@ -1066,7 +1335,7 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
       for (int n = slot; n < NLr; n += nslots)
 #pragma unroll
         for (int i = 0; i < I; ++i) {
-          const C2 z = ys[(n * G + g) * RS + i];
+          const C2 z = ys[slab_y<PAIRS>(n, g, i, G, RS)];
           psum += z.x * z.x + z.y * z.y;
         }
     const R pv[1] = {psum};
@@ -1101,6 +1370,11 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
   pw.gslab = !resident;
   pw.g = g; pw.J = J; pw.JS = JS; pw.rec0 = rec0; pw.rstep = rstep; pw.npts = npts;
   pw.wfl = wfl; pw.invI = invI;
+  {  // frame pairs: this thread's full pairs m = slot, slot + nslots, ... < NLr / 2, and the half pair
+    const int np = NLr >> 1;
+    pw.nfull = active ? (np > slot ? (np - slot + nslots - 1) / nslots : 0) : 0;
+    pw.part = active && (NLr & 1) && slot == np % nslots;
+  }
 
   // accumulator unit of this lane in the I > 4 phase B: a complex entry (x, y < x) of the packed
   // lower triangle, or a pair of diagonal entries (2d, 2d + 1)
@@ -1133,7 +1407,15 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
 #pragma unroll
       for (int k = 0; k < VA; ++k) acc[k] = R(0);
       const R vfl_b = R(vfl[g]);
-      if constexpr (PREG) {
+      if constexpr (PAIRS) {
+        if (rec) {
+          if (vf2) pw.template phaseA_pairs<true, true>(acc, vfl_b);
+          else pw.template phaseA_pairs<true, false>(acc, vfl_b);
+        } else {
+          if (vf2) pw.template phaseA_pairs<false, true>(acc, vfl_b);
+          else pw.template phaseA_pairs<false, false>(acc, vfl_b);
+        }
+      } else if constexpr (PREG) {
         if (rec) {
           if (vf2) pw.template phaseA<true, true>(acc, vfl_b);
           else pw.template phaseA<true, false>(acc, vfl_b);
@@ -1231,8 +1513,13 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
       R acc[NB + 1];
 #pragma unroll
       for (int k = 0; k < NB + 1; ++k) acc[k] = R(0);
-      if (rec && ch == 0) pw.template phaseB<true>(acc, ch);
-      else pw.template phaseB<false>(acc, ch);
+      if constexpr (PAIRS) {
+        if (rec) pw.template phaseB_pairs<true>(acc);
+        else pw.template phaseB_pairs<false>(acc);
+      } else {
+        if (rec && ch == 0) pw.template phaseB<true>(acc, ch);
+        else pw.template phaseB<false>(acc, ch);
+      }
       FFCA_PROBE(3)
       bin_reduce<R, NB + 1, G, SEG>(acc, wpart, cpart, tot, C, VMAX, parity);
       if (rec && ch == 0 && tid < G) llB = tot[tid * VMAX + NB];
@@ -1252,8 +1539,13 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
       const bool bact = gg < G && b < a.total_bins;
       double2* Ms = Msys + gg * (I + 1) * I * I;  // LU(P) + reciprocal pivots
       int* pv = pivs + gg * (I + 1) * I;
-      SmallLDL<I> ldl;
+      // I <= 3: B_i^-1 through its adjugate (a shallow dependency chain); I = 4: L D L^H
+      std::conditional_t<(I <= 3), HermAdj<I>, SmallLDL<I>> ldl;
+#ifdef FFCA_EXP_SKIP_SOLVE  // timing experiment only: P is never updated (results are wrong)
+      if (false) {
+#else
       if (bact && s > 0) {
+#endif
         const int i = s - 1;
         const double* T = tot + gg * VMAX + i * I * I;  // the reduced sums, published by bin_reduce
         double2 B[I][I];
@@ -1278,8 +1570,12 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
         }
       }
       FFCA_PROBE(5)
+#ifdef FFCA_EXP_SKIP_SOLVE
+      for (int k = 0; k < 0; ++k) {
+#else
 #pragma unroll 1
       for (int k = 0; k < a.K; ++k) {
+#endif
         if constexpr (I <= 4) {
           // Measured: a divergent LU thread and the LDL threads of one warp ran serially
           // (11 % of the iteration at I = 3, 13 % at I = 4).  An exactly zero determinant flags
@@ -1309,6 +1605,7 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
             for (int x = 0; x < I; ++x) det = cadd(det, cmul(Pb[x * I], c0[x]));
           }
           __syncwarp();  // every column is read before any thread writes its new one
+          FFCA_PROBE(6)
           if (bact && s > 0) {
             const int i = s - 1;
             if (det.x == 0.0 && det.y == 0.0) {
@@ -1406,7 +1703,8 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
   if (rec) {
     pw.load_PL();
     R acc[1] = {R(0)};
-    pw.phaseL(acc);
+    if constexpr (PAIRS) pw.phaseL_pairs(acc);
+    else pw.phaseL(acc);
     bin_reduce<R, 1, G, SEG>(acc, wpart, cpart, tot, C, VMAX, parity);
     if (tid < G) {
       const long long b = group * G + tid;
@@ -1423,8 +1721,10 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
   FFCA_FIXED(1)
   R* vo = (R*)a.v_out;
   if (active)
-    for (int j = 0; j < J; ++j)
-      for (int n = slot; n < NLr; n += nslots) vo[((u * J + j) * (long long)N + n0 + n) * F + f] = vs[(n * G + g) * JS + j];
+    for (int j = 0; j < J; ++j) {
+      R* col = vo + ((u * J + j) * (long long)N + n0) * F + f;
+      for (int n = slot; n < NLr; n += nslots) col[(long long)n * F] = vs[slab_v<PAIRS>(n, g, j, G, JS)];
+    }
   if (crank == 0) {
     for (int t = tid; t < G * I * I; t += blockDim.x) {
       const long long b = group * G + t / (I * I);

@@ -3,6 +3,8 @@ import dataclasses, json, os, sys
 sys.path.insert(0, os.path.abspath(os.path.join(os.path.dirname(__file__), "..")))
 import torch
 from paper_1805_09498_b200 import _lib
+if os.environ.get("FFCA_LIB"):  # an experiment build (e.g. build/libffca_exp1.so)
+    _lib.LIB_PATH = os.environ["FFCA_LIB"]
 from paper_1805_09498_b200.workloads import CONFIGS, make_torch
 
 cid = int(sys.argv[1]) if len(sys.argv) > 1 else 4

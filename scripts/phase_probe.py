@@ -27,7 +27,7 @@ for rep in range(2):
         print("note: call returned", rc, _lib.last_error())
     torch.cuda.synchronize()
 lib.ffca_debug_phase(out.ctypes.data)
-names = ["A points", "A reduce", "lambda'+bar", "B points", "B reduce+bar", "B_i factor (LDL)", "P^-1 (K > 1)", "solve+bar"]
+names = ["A points", "A reduce", "lambda'+bar", "B points", "B reduce+bar", "B_i factor", "adj(P), det (I<=4)", "solve+bar"]
 for t in range(2):
     tot = out[8 * t: 8 * t + 8].astype(float)
     print(f"thread {t}: total {tot.sum() / cfg.iterations:.0f} cycles/iteration")
