@@ -57,17 +57,60 @@ int reduce_ll(const double* ll_bins, double* ll_mix_dev, int U, int F, int nev, 
   return FFCA_OK;
 }
 
+// OR of all per-bin status words and the first bin carrying a fatal bit (order independent, so
+// deterministic): out[0] = OR, out[1] = first fatal bin or INT_MAX.
+__global__ void status_summary_kernel(const int* st, long long n, int fatal_mask, int* out) {
+  __shared__ int s_or, s_first;
+  if (threadIdx.x == 0) {
+    s_or = 0;
+    s_first = 0x7fffffff;
+  }
+  __syncthreads();
+  int o = 0, fst = 0x7fffffff;
+  for (long long k = threadIdx.x; k < n; k += blockDim.x) {
+    const int v = st[k];
+    o |= v;
+    if ((v & fatal_mask) && k < fst) fst = int(k);
+  }
+  atomicOr(&s_or, o);
+  atomicMin(&s_first, fst);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    out[0] = s_or;
+    out[1] = s_first;
+  }
+}
+
 int finish_status(const int* status_dev, int* status_user, long long nbins, int mem, cudaStream_t s,
                   int fatal_mask) {
   if (nbins == 0) return FFCA_OK;
-  std::vector<int> h(nbins);
-  FFCA_CK(cudaMemcpyAsync(h.data(), status_dev, nbins * sizeof(int), cudaMemcpyDeviceToHost, s));
-  FFCA_CK(cudaStreamSynchronize(s));
   int any = 0;
   long long first = -1;
-  for (long long k = 0; k < nbins; ++k) {
-    any |= h[k];
-    if (first < 0 && (h[k] & fatal_mask)) first = k;
+  std::vector<int> h;
+  if (status_user && mem != FFCA_MEM_DEVICE) {  // the caller wants every bin's word on the host
+    h.resize(nbins);
+    FFCA_CK(cudaMemcpyAsync(h.data(), status_dev, nbins * sizeof(int), cudaMemcpyDeviceToHost, s));
+    FFCA_CK(cudaStreamSynchronize(s));
+    for (long long k = 0; k < nbins; ++k) {
+      any |= h[k];
+      if (first < 0 && (h[k] & fatal_mask)) first = k;
+    }
+  } else {  // summarise on the device: 8 bytes back instead of the whole status array
+    int* d2 = nullptr;
+    FFCA_CK(cudaMallocAsync(&d2, 2 * sizeof(int), s));
+    status_summary_kernel<<<1, 1024, 0, s>>>(status_dev, nbins, fatal_mask, d2);
+    count_launch();
+    int h2[2] = {0, 0};
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h2, d2, sizeof(h2), cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(d2, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      set_error("status summary: %s", cudaGetErrorString(e));
+      return FFCA_E_CUDA;
+    }
+    any = h2[0];
+    first = h2[1] == 0x7fffffff ? -1 : h2[1];
   }
   if (status_user) {
     if (mem == FFCA_MEM_DEVICE)

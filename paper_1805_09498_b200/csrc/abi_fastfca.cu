@@ -3,6 +3,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "ffca_loop.cuh"
@@ -154,9 +156,38 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
   return FFCA_OK;
 }
 
-static int launch_loop(LoopFn fn, const LoopPlan& p, const LoopArgs& a, cudaStream_t s) {
-  FFCA_CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p.smem)));
-  if (p.C > 8) FFCA_CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+// Per-device attributes and per-kernel shared-memory opt-ins, set once (the calls cost a few
+// microseconds each -- 10-20 % of a config-0 call).
+struct DevAttrs {
+  int optin = 0, nsm = 0;
+};
+static int device_attrs(int device, DevAttrs& out) {
+  static std::mutex mu;
+  static DevAttrs cache[64];
+  std::lock_guard<std::mutex> lk(mu);
+  if (device < 0 || device >= 64) return FFCA_E_ARG;
+  if (cache[device].nsm == 0) {
+    FFCA_CK(cudaDeviceGetAttribute(&cache[device].optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    FFCA_CK(cudaDeviceGetAttribute(&cache[device].nsm, cudaDevAttrMultiProcessorCount, device));
+  }
+  out = cache[device];
+  return FFCA_OK;
+}
+static int func_smem_optin(LoopFn fn, int device, size_t smem, bool nonportable) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;  // (kernel, device) -> opted-in bytes
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[{(const void*)fn, device}];
+  if (smem > have) {
+    FFCA_CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    have = smem;
+  }
+  if (nonportable) FFCA_CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  return FFCA_OK;
+}
+
+static int launch_loop(LoopFn fn, const LoopPlan& p, const LoopArgs& a, cudaStream_t s, int device) {
+  FFCA_TRY(func_smem_optin(fn, device, p.smem, p.C > 8));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(p.grid), 1, 1);
   cfg.blockDim = dim3(unsigned(p.threads), 1, 1);
@@ -197,12 +228,10 @@ struct DevProblem {
 static int launch_problem(int device, const DevProblem& d, cudaStream_t s) {
   const long long nb = (long long)d.U * d.F;
   if (nb == 0) return FFCA_OK;
-  int optin = 0;
-  FFCA_CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-  int nsm = 148;
-  FFCA_CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+  DevAttrs da;
+  FFCA_TRY(device_attrs(device, da));
   LoopPlan p;
-  FFCA_TRY(plan_loop(d.dtype, d.I, d.J, d.N, nb, d.vf_mode, p, size_t(optin), nsm));
+  FFCA_TRY(plan_loop(d.dtype, d.I, d.J, d.N, nb, d.vf_mode, p, size_t(da.optin), da.nsm));
   void* scratch = nullptr;
   if (!p.resident) FFCA_CK(cudaMallocAsync(&scratch, size_t(p.grid) * p.slab, s));
   LoopArgs a;
@@ -268,7 +297,7 @@ static int launch_problem(int device, const DevProblem& d, cudaStream_t s) {
     count_launch();
     a.packed = packed;
   }
-  FFCA_TRY(launch_loop(fn, p, a, s));
+  FFCA_TRY(launch_loop(fn, p, a, s, device));
   FFCA_CK(cudaGetLastError());
   if (ev0) {
     FFCA_CK(cudaEventRecord(ev1, s));

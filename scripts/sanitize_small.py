@@ -24,7 +24,10 @@ def run(I, J, F, N, c64=False, plan=None, it=2, rank=4, zf=0.0):
     print("ok", I, J, F, N, c64, plan, flush=True)
 
 
-run(3, 3, 9, 40, c64=True)                 # G=4 resident
+run(3, 3, 9, 40, c64=True)                 # c64 I=J=3: 2-bin CTAs, frame-pair records
+run(3, 3, 9, 41, c64=True)                 # odd frame count: the half-filled last pair
+run(3, 3, 9, 41, c64=True, plan="1,2,1")   # frame pairs split over a cluster (odd per-rank counts)
+run(3, 3, 300, 30)                         # c128 one-bin CTAs with 16-lane reduction segments
 run(3, 3, 7, 40)                           # c128 G=2
 run(3, 3, 5, 90, c64=True, plan="1,2,1")   # cluster of 2
 run(4, 4, 5, 70, c64=True, plan="1,4,1")   # I=4 cluster of 4
