@@ -139,3 +139,21 @@ def test_batch_entry_validates_before_the_abi():
     short = (np.empty((2, 4, 3, 3), np.complex128), np.empty((2, 2, 4, 3)), np.empty((1, 2, 5, 4)))
     with pytest.raises(ValueError):
         fastfca.run_fastfca_batch(y, P0, lam0, v0, out=short)
+
+
+def test_cli_device_option_parsing():
+    from paper_1805_09498_b200 import cli as dev_cli
+
+    class Fake:  # stands in for fcasep.cli: records the argv it is handed and the installed hooks
+        _run_estimator = _images_from_run = None
+
+        @staticmethod
+        def main(argv):
+            Fake.argv = argv
+            return 0
+
+    assert dev_cli.main(["bench", "--device", "tpu"], cli_module=Fake) == 2
+    assert dev_cli.main(["bench", "--device=cpu", "--trials", "2"], cli_module=Fake) == 0
+    assert Fake.argv == ["bench", "--trials", "2"] and Fake._run_estimator is None
+    assert dev_cli.main(["separate", "--device", "cuda", "--iterations", "3"], cli_module=Fake) == 0
+    assert Fake.argv == ["separate", "--iterations", "3"] and Fake._run_estimator is dev_cli.run_estimator
