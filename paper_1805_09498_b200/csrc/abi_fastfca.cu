@@ -14,8 +14,8 @@
 namespace ffca {
 
 using LoopFn = void (*)(const LoopArgs);
-LoopFn loop_kernel_f32(int I, int J, int G, bool res);
-LoopFn loop_kernel_f64(int I, int J, int G, bool res);
+LoopFn loop_kernel_f32(int I, int J, int G, bool res, bool fast);
+LoopFn loop_kernel_f64(int I, int J, int G, bool res, bool fast);
 
 static bool hot_shape(int I, int J) {
   return (I == 3 && J == 3) || (I == 4 && J == 4) || (I == 8 && J == 6) || (I == 2 && J == 2);
@@ -249,8 +249,10 @@ static int launch_problem(int device, const DevProblem& d, cudaStream_t s) {
   a.slab_bytes = (long long)p.slab;
   a.packed = nullptr;
   a.L = p.L;
-  LoopFn fn = d.dtype == FFCA_C64 ? loop_kernel_f32(d.I, d.J, p.G, p.resident)
-                                  : loop_kernel_f64(d.I, d.J, p.G, p.resident);
+  // the plain loop (no likelihood, no full floor array, no P-only pass, K = 1) has lean instantiations
+  const bool fast = d.ll_bins == nullptr && d.vf_mode != 2 && !d.p_only && d.K == 1 && !getenv("FFCA_NO_FAST");
+  LoopFn fn = d.dtype == FFCA_C64 ? loop_kernel_f32(d.I, d.J, p.G, p.resident, fast)
+                                  : loop_kernel_f64(d.I, d.J, p.G, p.resident, fast);
   if (!fn) {
     set_error("no kernel for I=%d J=%d", d.I, d.J);
     return FFCA_E_UNSUPPORTED;

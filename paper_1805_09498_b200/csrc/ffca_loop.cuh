@@ -1159,7 +1159,10 @@ __global__ void __launch_bounds__(256) slab_pack_kernel(const PackArgs a) {
   }
 }
 
-template <typename R, int I, int JT, int G, bool RES>
+// FAST: the plain estimation loop (no likelihood recording, no full floor array, no P-only pass,
+// one inner iteration) -- those paths compile out, which keeps the hot instantiations smaller
+// (instruction cache) and lighter on registers.  The launcher picks it when a call allows.
+template <typename R, int I, int JT, int G, bool RES, bool FAST = false>
 __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffca_loop_kernel(const LoopArgs a) {
   using C2 = typename Cpx<R>::T;
   constexpr int JM = JT > 0 ? JT : 8;
@@ -1243,6 +1246,7 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
   }
   if (!(a.packed && resident)) {
     const R* vfg = (const R*)a.vf;
+    const bool vf2g = !FAST && a.vf_mode == 2;
     if (resident) {
       // Pointer-bumped frame loops: iteration k copies frame slot + k * nslots (nslots is even, so
       // the slab offset advances by a constant in both record layouts); frames >= NLr zero-fill.
@@ -1265,7 +1269,7 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
         R* dst = vs + slab_v<PAIRS>(slot, g, j, G, JS);
 #pragma unroll 1
         for (int k = 0; k < nit; ++k, src += gstep, dst += vstep) cp_async<sizeof(R)>(dst, k < nok ? src : vg + c0, k < nok);
-        if (a.vf_mode == 2) {
+        if (vf2g) {
           const R* fsrc = vfg + c0 + (long long)slot * F;
           R* fdst = vfs + slab_v<PAIRS>(slot, g, j, G, JS);
 #pragma unroll 1
@@ -1284,7 +1288,7 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
           const bool ok = active && n < NLr;
           const long long off = ((u * J + j) * (long long)N + n0 + n) * F + f;
           vs[slab_v<PAIRS>(n, g, j, G, JS)] = ok ? vg[off] : R(0);
-          if (a.vf_mode == 2) vfs[slab_v<PAIRS>(n, g, j, G, JS)] = ok ? vfg[off] : R(0);
+          if (vf2g) vfs[slab_v<PAIRS>(n, g, j, G, JS)] = ok ? vfg[off] : R(0);
         }
     }
   }
@@ -1355,8 +1359,9 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
   }
   __syncthreads();
 
-  const bool rec = a.ll != nullptr;
-  const bool vf2 = a.vf_mode == 2;
+  const bool rec = !FAST && a.ll != nullptr;
+  const bool vf2 = !FAST && a.vf_mode == 2;
+  const int KK = FAST ? 1 : a.K;
   const int nev = 1 + 2 * a.iters;
   const R wfl = Floors<R>::weight;
   const R invI = R(1) / R(I);
@@ -1401,7 +1406,7 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
   for (int it = 0; it < a.iters; ++it) {
     // ---------------- phase A: fused E/M sweep ----------------
     double llA = 0.0;
-    if (!a.p_only) {
+    if (FAST || !a.p_only) {
       pw.load_PL();
       R acc[VA];
 #pragma unroll
@@ -1574,7 +1579,7 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
       for (int k = 0; k < 0; ++k) {
 #else
 #pragma unroll 1
-      for (int k = 0; k < a.K; ++k) {
+      for (int k = 0; k < KK; ++k) {
 #endif
         if constexpr (I <= 4) {
           // Measured: a divergent LU thread and the LDL threads of one warp ran serially
@@ -1665,7 +1670,7 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
       }
       FFCA_PROBE(5)
 #pragma unroll 1
-      for (int k = 0; k < a.K; ++k) {
+      for (int k = 0; k < KK; ++k) {
         if (k > 0) {
           if ((tid >> 3) == mP) invert_P_group<I>(Pd, Pinv, rhsv, tid & 7, false, ldet, a.status, group, active && crank == 0);
           __syncthreads();

@@ -704,3 +704,40 @@ def test_loading_retry_is_per_bin_documented_divergence(monkeypatch):
     others = [0, 2, 3, 4]
     d = np.abs(P[others] - whole.P[others]).max() / np.abs(whole.P[others]).max()
     assert 0.0 < d <= 1e-8  # the whole-batch retry also loaded the healthy bins (by ~1e-10 tr)
+
+
+@pytest.mark.parametrize("dt,shape", [("c64", (3, 3, 40, 90)), ("c128", (3, 3, 40, 90)), ("c64", (4, 4, 6, 700)),
+                                      ("c64", (8, 6, 3, 160))])
+def test_lean_instantiation_matches_general(dt, shape):
+    # the plain loop runs lean (FAST) instantiations with the likelihood / floor-array / P-only paths
+    # compiled out.  They are separate compilations of the same arithmetic, so nvcc may contract a
+    # different a*b + c*d into an FMA: the state agrees with the general kernel (FFCA_NO_FAST=1, or a
+    # call that records the likelihood) to rounding, not necessarily bitwise
+    I, J, F, N = shape
+    y, P0, lam0, v0, _ = mixture(91, I, J, F, N, 4, 0.05 if I > 4 else 0.0)
+    y, P0, lam0, v0 = cast(dt, y, P0, lam0, v0)
+    args = (y[None], P0[None], lam0[None], v0[None])
+    fast = fastfca.run_fastfca_batch(*args, iterations=5)
+    rec = fastfca.run_fastfca_batch(*args, iterations=5, record_likelihood=True)
+    os.environ["FFCA_NO_FAST"] = "1"
+    try:
+        general = fastfca.run_fastfca_batch(*args, iterations=5)
+    finally:
+        os.environ.pop("FFCA_NO_FAST")
+    tol = 1e-12 if dt == "c128" else 1e-5
+    for a, b, c in zip(fast[:3], rec[:3], general[:3]):
+        assert rel(a, c) <= tol and rel(b, c) <= tol
+
+
+def test_c128_lean_results_do_not_depend_on_batch_size():
+    # the bitwise batch-size independence of the complex128 plans also holds for the lean kernels
+    cfg = CONFIGS[0]
+    args = _stack(range(540, 544), cfg.I, cfg.J, cfg.F, cfg.N)
+    os.environ["FFCA_NO_PIPELINE"] = "1"
+    try:
+        batch = fastfca.run_fastfca_batch(*args, iterations=5)
+        one = fastfca.run_fastfca_batch(*(a[2:3] for a in args), iterations=5)
+    finally:
+        os.environ.pop("FFCA_NO_PIPELINE")
+    for a, b in zip(one[:3], batch[:3]):
+        assert np.array_equal(a[0], b[2])
