@@ -1173,7 +1173,7 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
   constexpr int VA = JM * (1 + I) + 1;
   const int J = JT > 0 ? JT : a.J;
   const int JS = loop_js(I, JM, J);
-  const int C = a.C;
+  const int C = G > 1 ? 1 : a.C;  // multi-bin groups never form clusters (plan_loop): the DSMEM paths compile out
   const int tid = threadIdx.x;
   const int g = tid % G;
   const int slot = tid / G, nslots = blockDim.x / G;
