@@ -738,25 +738,37 @@ struct PointWork {
     acc[NB] = lacc;
   }
 
-  // Phase B for I > 4 as a skinny GEMM over the frames: B_i[e] = sum_n Z_e(n) / w_i(n), with
-  // Z_e = y_a conj(y_b).  A warp walks chunks of 32 frames (chunk c of the CTA belongs to warp
-  // c % W): lane l first forms the I reciprocal weights of frame 32c + l (and, with REC, its
-  // likelihood terms) into the warp's buffer, then every lane accumulates its own unit -- one
-  // complex entry (ua > ub) or two diagonal entries (ua, ub) -- against all I weights of each
-  // frame: two y loads, one product and I FFMA2 per lane and frame, no cross-lane reduction.
-  // Frames past the bin's range get zero weights (their records are zero-filled or clamped).
+  // Phase B for I > 4 with two accumulator units per lane: lanes l and l + 16 own units l and
+  // l + 16 (of the 32) and walk alternate frames of each 32-frame chunk (half h = l / 16 takes
+  // frames h, h + 2, ...), so every weight load and loop step feeds 16 FFMA2 instead of 8; the two
+  // halves' sums are folded with one shuffle at the end.  Same per-unit arithmetic as the one-unit
+  // form (measured at config 4: 14.91 -> 14.56 ms).
+  __device__ __forceinline__ C2 unit_z(const C2* rec, int ua, int ub, bool diag) const {
+    // z = U V + X Z:
+    // complex unit  ya conj(yb):  U = (ya.x, ya.y), V = (yb.x, yb.x), X = (ya.y, -ya.x), Z = (yb.y, yb.y)
+    // diagonal pair (|ya|^2, |yb|^2): U = V = (ya.x, yb.x), X = Z = (ya.y, yb.y)
+    const C2 ya = rec[ua], yb = rec[ub];
+    const C2 U = mk<C2, R>(ya.x, diag ? yb.x : ya.y);
+    const C2 V = mk<C2, R>(diag ? ya.x : yb.x, yb.x);
+    const C2 X = mk<C2, R>(ya.y, diag ? yb.y : -ya.x);
+    const C2 Z = mk<C2, R>(diag ? ya.y : yb.y, yb.y);
+    return fma2(U, V, fma2(X, Z, mk<C2, R>(R(0), R(0))));
+  }
   template <bool REC>
-  __device__ __forceinline__ void phaseB_entry(C2 (&ac)[I], R& lacc, int NLr, bool active, R* wbuf, int ua, int ub,
-                                               bool diag, int c0, int cstep) const {
+  __device__ __forceinline__ void phaseB_entry(C2 (&ac)[2][I], R& lacc, int NLr, bool active, R* wbuf,
+                                               const int (&ua)[2], const int (&ub)[2], const bool (&dg)[2], int c0,
+                                               int cstep) const {
     constexpr int IWS = Shape<I, JM>::IWS;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, h = lane >> 4;
     R lam[JM][I];
 #pragma unroll
     for (int j = 0; j < JM; ++j)
 #pragma unroll
       for (int i = 0; i < I; ++i) lam[j][i] = (j < J) ? lamc[j * I + i] : R(0);
 #pragma unroll
-    for (int i = 0; i < I; ++i) ac[i] = mk<C2, R>(R(0), R(0));
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int i = 0; i < I; ++i) ac[k][i] = mk<C2, R>(R(0), R(0));
     const int nch = active ? (NLr + 31) / 32 : 0;
 #pragma unroll 1
     for (int c = c0; c < nch; c += cstep) {
@@ -804,25 +816,30 @@ struct PointWork {
       }
       __syncwarp();
       const int nf = min(32, NLr - 32 * c);
-      const C2* rec = ys + (32 * c) * RS;
-#pragma unroll 4
-      for (int f = 0; f < nf; ++f, rec += RS) {
-        const C2 ya = rec[ua], yb = rec[ub];
-        // z = U V + X Z (two packed FMAs, the same for every lane; the FMA pipe is the bound):
-        // complex unit  ya conj(yb):  U = (ya.x, ya.y), V = (yb.x, yb.x), X = (ya.y, -ya.x), Z = (yb.y, yb.y)
-        // diagonal pair (|ya|^2, |yb|^2): U = V = (ya.x, yb.x), X = Z = (ya.y, yb.y)
-        const C2 U = mk<C2, R>(ya.x, diag ? yb.x : ya.y);
-        const C2 V = mk<C2, R>(diag ? ya.x : yb.x, yb.x);
-        const C2 X = mk<C2, R>(ya.y, diag ? yb.y : -ya.x);
-        const C2 Z = mk<C2, R>(diag ? ya.y : yb.y, yb.y);
-        const C2 z = fma2(U, V, fma2(X, Z, mk<C2, R>(R(0), R(0))));
+      const C2* rec = ys + (32 * c + h) * RS;
+      const R* wq = wbuf + h * IWS;
+#pragma unroll 2
+      for (int f = h; f < nf; f += 2, rec += 2 * RS, wq += 2 * IWS) {
+        // units 0..15 are complex entries whenever I >= 7 (NCX >= 16): no diagonal selects
+        const C2 z0 = unit_z(rec, ua[0], ub[0], Shape<I, JM>::NCX >= 16 ? false : dg[0]);
+        const C2 z1 = unit_z(rec, ua[1], ub[1], dg[1]);
         R wv[IWS];
-        load_vec<IWS>(wbuf + f * IWS, wv);
+        load_vec<IWS>(wq, wv);
 #pragma unroll
-        for (int i = 0; i < I; ++i) ac[i] = fma2(z, bc2<R>(wv[i]), ac[i]);
+        for (int i = 0; i < I; ++i) {
+          ac[0][i] = fma2(z0, bc2<R>(wv[i]), ac[0][i]);
+          ac[1][i] = fma2(z1, bc2<R>(wv[i]), ac[1][i]);
+        }
       }
       __syncwarp();
     }
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int i = 0; i < I; ++i) {
+        ac[k][i].x += __shfl_xor_sync(FULL, ac[k][i].x, 16);
+        ac[k][i].y += __shfl_xor_sync(FULL, ac[k][i].y, 16);
+      }
   }
 
   // ---------------- frame-pair point work (PAIRS: complex64, I <= 4) ----------------
@@ -1383,21 +1400,25 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
 
   // accumulator unit of this lane in the I > 4 phase B: a complex entry (x, y < x) of the packed
   // lower triangle, or a pair of diagonal entries (2d, 2d + 1)
-  int bua = 0, bub = 0;
-  bool bdiag = false, bown = false;
+  // (two units per lane: lanes l and l + 16 both hold units l and l + 16, on alternate frames)
+  int bua[2] = {0, 0}, bub[2] = {0, 0};
+  bool bdiag[2] = {false, false}, bown[2] = {false, false};
   if constexpr (Shape<I, JM>::GROUPB) {
-    const int u = tid & 31;
-    bown = u < Shape<I, JM>::NU;
-    if (u < Shape<I, JM>::NCX) {
-      int x = 1;
-      while ((x + 1) * x / 2 <= u) ++x;
-      bua = x;
-      bub = u - x * (x - 1) / 2;
-    } else if (bown) {
-      const int d = u - Shape<I, JM>::NCX;
-      bdiag = true;
-      bua = 2 * d;
-      bub = 2 * d + 1 < I ? 2 * d + 1 : 2 * d;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int u = (tid & 15) + 16 * k;
+      bown[k] = u < Shape<I, JM>::NU;
+      if (u < Shape<I, JM>::NCX) {
+        int x = 1;
+        while ((x + 1) * x / 2 <= u) ++x;
+        bua[k] = x;
+        bub[k] = u - x * (x - 1) / 2;
+      } else if (bown[k]) {
+        const int d = u - Shape<I, JM>::NCX;
+        bdiag[k] = true;
+        bua[k] = 2 * d;
+        bub[k] = 2 * d + 1 < I ? 2 * d + 1 : 2 * d;
+      }
     }
   }
 
@@ -1472,9 +1493,11 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
       // The last warp inverts P meanwhile (8-lane Gauss-Jordan, partial pivoting: P does not
       // change before the solve), so P^-1 is off the per-iteration critical path; the other
       // W - 1 warps share the frames.
-      C2 bac[I];
+      C2 bac[2][I];
 #pragma unroll
-      for (int i = 0; i < I; ++i) bac[i] = mk<C2, R>(R(0), R(0));
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int i = 0; i < I; ++i) bac[k][i] = mk<C2, R>(R(0), R(0));
       R lacc = R(0);
       const int warp = tid >> 5;
       if (warp == W - 1) {
@@ -1493,20 +1516,24 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
       __syncthreads();  // every warp is done with its weight buffer (it aliases the partials)
       {
         R* wp = wpart + (tid >> 5) * VMAX;
-        if (bdiag) {
+        if ((tid & 31) < 16)  // the folded sums (lanes l + 16 hold the same)
 #pragma unroll
-          for (int i = 0; i < I; ++i) {
-            wp[i * I * I + bua * bua] = bac[i].x;
-            if (bub != bua) wp[i * I * I + bub * bub] = bac[i].y;
-          }
-        } else if (bown) {
-          const int e = bua * bua + 1 + 2 * bub;
+          for (int k = 0; k < 2; ++k) {
+            if (bdiag[k]) {
 #pragma unroll
-          for (int i = 0; i < I; ++i) {
-            wp[i * I * I + e] = bac[i].x;
-            wp[i * I * I + e + 1] = bac[i].y;
+              for (int i = 0; i < I; ++i) {
+                wp[i * I * I + bua[k] * bua[k]] = bac[k][i].x;
+                if (bub[k] != bua[k]) wp[i * I * I + bub[k] * bub[k]] = bac[k][i].y;
+              }
+            } else if (bown[k]) {
+              const int e = bua[k] * bua[k] + 1 + 2 * bub[k];
+#pragma unroll
+              for (int i = 0; i < I; ++i) {
+                wp[i * I * I + e] = bac[k][i].x;
+                wp[i * I * I + e + 1] = bac[k][i].y;
+              }
+            }
           }
-        }
         if ((tid & 31) == 0) wp[I * I * I] = lacc;
       }
       bin_reduce_tail<G>(I * I * I + 1, wpart, cpart, tot, C, VMAX, parity);

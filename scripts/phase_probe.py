@@ -6,7 +6,7 @@ sys.path.insert(0, ROOT)
 import numpy as np
 import torch
 from paper_1805_09498_b200 import _lib
-_lib.LIB_PATH = os.path.join(ROOT, "build", "libffca_probe.so")
+_lib.LIB_PATH = os.environ.get("FFCA_PROBE_LIB", os.path.join(ROOT, "build", "libffca_probe.so"))
 from paper_1805_09498_b200.workloads import CONFIGS, make_torch
 
 cfg = CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 3]
