@@ -1,6 +1,9 @@
 mkdir -p gpurun_out
 {
-python scripts/exp_time.py 3
-python scripts/exp_time.py 4
-} > gpurun_out/exp5.log 2>&1
-python -m pytest tests -m gpu -x -q > gpurun_out/exp_tests.log 2>&1; echo "pytest rc=$?" >> gpurun_out/exp_tests.log
+python scripts/fixed_probe.py 4 0
+python scripts/fixed_probe.py 4 20
+python scripts/fixed_probe.py 3 0
+python scripts/fixed_probe.py 3 20
+python scripts/fixed_probe.py 2 0
+python scripts/fixed_probe.py 2 30
+} > gpurun_out/fixed.log 2>&1
