@@ -39,6 +39,9 @@ extern "C" {
 
 #define FFCA_MEM_HOST 0
 #define FFCA_MEM_DEVICE 1
+/* ffca_fastfca_run_stats only: host arrays, except mu_out / phi_out, which are device memory
+ * (the statistics stay in HBM for a device consumer, e.g. the Wiener images) */
+#define FFCA_MEM_HOST_STATS_DEVICE 2
 
 /* v_floor modes (fastfca.py:406,421-424,435-436) */
 #define FFCA_VF_SCALAR 0 /* v_floor is a python float               */
@@ -91,7 +94,8 @@ int ffca_fastfca_run(int device, void* stream, int mem, int dtype, int U, int I,
  * :373-387): after the loop kernel the per-point refresh runs on the
  * device-resident final state; mu_out (U, J, N, F, I) complex, phi_out
  * (U, J, N, F, I) real, either may be NULL.  Host mode moves both outputs
- * chunk by chunk, overlapped with the next chunk's loop.
+ * chunk by chunk, overlapped with the next chunk's loop; FFCA_MEM_HOST_STATS_DEVICE
+ * writes them into device buffers instead (nothing crosses PCIe for them).
  */
 int ffca_fastfca_run_stats(int device, void* stream, int mem, int dtype, int U, int I, int J, int N, int F,
                            const void* y, const void* P0, const void* lam0, const void* v0, int vf_mode,

@@ -23,7 +23,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FFCA_LIB", os.path.join(_HERE, "libffca_b200.so"))
 
 C128, C64 = 0, 1
-MEM_HOST, MEM_DEVICE = 0, 1
+MEM_HOST, MEM_DEVICE, MEM_HOST_STATS_DEVICE = 0, 1, 2
 VF_SCALAR, VF_BIN, VF_FULL, VF_AUTO = 0, 1, 2, 3
 
 OK, E_ARG, E_CUDA, E_SINGULAR_P, E_SINGULAR_B, E_NOT_PD, E_UNSUPPORTED = 0, -1, -2, -3, -4, -5, -6

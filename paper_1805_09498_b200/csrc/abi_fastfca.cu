@@ -331,8 +331,9 @@ struct Blk {
 };
 
 static int copy_blk(void* dst, const void* src, const Blk& b, int U, int F, int u0, int Uc, int f0, int Fc,
-                    bool h2d, cudaStream_t s) {
+                    bool h2d, cudaStream_t s, bool d2d = false) {
   if (!dst || !src) return FFCA_OK;
+  const cudaMemcpyKind out_kind = d2d ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
   const size_t pitch_full = size_t(F) * b.B * b.es, width = size_t(Fc) * b.B * b.es;
   const size_t off = ((size_t(u0) * b.A) * F + f0) * b.B * b.es;
   if (width == pitch_full) {  // whole rows: one linear copy
@@ -340,15 +341,14 @@ static int copy_blk(void* dst, const void* src, const Blk& b, int U, int F, int 
     if (h2d)
       FFCA_CK(cudaMemcpyAsync(dst, (const char*)src + off, n, cudaMemcpyHostToDevice, s));
     else
-      FFCA_CK(cudaMemcpyAsync((char*)dst + off, src, n, cudaMemcpyDeviceToHost, s));
+      FFCA_CK(cudaMemcpyAsync((char*)dst + off, src, n, out_kind, s));
     return FFCA_OK;
   }
   if (h2d)
     FFCA_CK(cudaMemcpy2DAsync(dst, width, (const char*)src + off, pitch_full, width, size_t(Uc) * b.A,
                               cudaMemcpyHostToDevice, s));
   else
-    FFCA_CK(cudaMemcpy2DAsync((char*)dst + off, pitch_full, src, width, width, size_t(Uc) * b.A,
-                              cudaMemcpyDeviceToHost, s));
+    FFCA_CK(cudaMemcpy2DAsync((char*)dst + off, pitch_full, src, width, width, size_t(Uc) * b.A, out_kind, s));
   (void)U;
   return FFCA_OK;
 }
@@ -368,7 +368,7 @@ struct PipeRes {
 };
 
 static int pipelined_body(PipeRes& R, int device, cudaStream_t user, const DevProblem& proto, bool rec, int nchunk,
-                          bool by_mixture,
+                          bool by_mixture, bool stats_dev,
                           const void* y, const void* P0, const void* lam0, const void* v0, const void* vf,
                           void* P_out, void* lam_out, void* v_out, double* ll_out, double* vf_out,
                           int* status_out, void* mu_out, void* phi_out) {
@@ -438,8 +438,9 @@ static int pipelined_body(PipeRes& R, int device, cudaStream_t user, const DevPr
     if (!rc && vf_out) rc = dalloc(bytes(Bvo), &dvo[k]);
     if (!rc && !by_mixture) rc = dalloc(bytes(Bst), &dst[k]);
     if (!rc && rec && !by_mixture) rc = dalloc(bytes(Bll), &dll[k]);
-    if (!rc && mu_out) rc = dalloc(bytes(Bmu), &dmu[k]);
-    if (!rc && phi_out) rc = dalloc(bytes(Bphi), &dphi[k]);
+    // device-resident statistics of mixture chunks are written in place (no chunk buffers)
+    if (!rc && mu_out && !(stats_dev && by_mixture)) rc = dalloc(bytes(Bmu), &dmu[k]);
+    if (!rc && phi_out && !(stats_dev && by_mixture)) rc = dalloc(bytes(Bphi), &dphi[k]);
   }
   int nch = 0;
   for (int c0 = 0; !rc && c0 < (by_mixture ? U : F); c0 += (by_mixture ? cu : cf), ++nch) {
@@ -468,6 +469,10 @@ static int pipelined_body(PipeRes& R, int device, cudaStream_t user, const DevPr
     d.mu = dmu[k]; d.phi = dphi[k];
     if (by_mixture) {  // views into the whole-batch buffers (mixture blocks are contiguous)
       const size_t b0 = size_t(u0) * F;
+      if (stats_dev) {
+        d.mu = mu_out ? (char*)mu_out + size_t(u0) * J * N * F * I * cs : nullptr;
+        d.phi = phi_out ? (char*)phi_out + size_t(u0) * J * N * F * I * rs : nullptr;
+      }
       d.P0 = (const char*)fP0 + b0 * I * I * cs;
       d.lam0 = (const char*)fl0 + size_t(u0) * J * F * I * rs;
       d.P = (char*)fP + b0 * I * I * cs;
@@ -500,8 +505,10 @@ static int pipelined_body(PipeRes& R, int device, cudaStream_t user, const DevPr
     }
     if (!rc) rc = copy_blk(v_out, dv[k], Bv, U, F, u0, Uc, f0, Fc, false, sout);
     if (!rc && vf_out) rc = copy_blk(vf_out, dvo[k], Bvo, U, F, u0, Uc, f0, Fc, false, sout);
-    if (!rc && mu_out) rc = copy_blk(mu_out, dmu[k], Bmu, U, F, u0, Uc, f0, Fc, false, sout);
-    if (!rc && phi_out) rc = copy_blk(phi_out, dphi[k], Bphi, U, F, u0, Uc, f0, Fc, false, sout);
+    if (!(stats_dev && by_mixture)) {
+      if (!rc && mu_out) rc = copy_blk(mu_out, dmu[k], Bmu, U, F, u0, Uc, f0, Fc, false, sout, stats_dev);
+      if (!rc && phi_out) rc = copy_blk(phi_out, dphi[k], Bphi, U, F, u0, Uc, f0, Fc, false, sout, stats_dev);
+    }
     if (!rc) FFCA_CK(cudaEventRecord(ev_out[k], sout));
   }
   if (!rc && by_mixture) {  // the whole-batch P / lambda after the last kernel
@@ -522,12 +529,12 @@ static int pipelined_body(PipeRes& R, int device, cudaStream_t user, const DevPr
 }
 
 static int pipelined_host_run(int device, cudaStream_t user, const DevProblem& proto, bool rec, int nchunk,
-                              bool by_mixture,
+                              bool by_mixture, bool stats_dev,
                               const void* y, const void* P0, const void* lam0, const void* v0, const void* vf,
                               void* P_out, void* lam_out, void* v_out, double* ll_out, double* vf_out,
                               int* status_out, void* mu_out, void* phi_out) {
   PipeRes R;
-  const int rc = pipelined_body(R, device, user, proto, rec, nchunk, by_mixture, y, P0, lam0, v0, vf, P_out,
+  const int rc = pipelined_body(R, device, user, proto, rec, nchunk, by_mixture, stats_dev, y, P0, lam0, v0, vf, P_out,
                                 lam_out, v_out, ll_out, vf_out, status_out, mu_out, phi_out);
   // Every path ends here.  Drain all three streams first: after a failure, H2D copies on sin and
   // D2H copies on sout may still be reading / writing the caller's host buffers and the device
@@ -553,6 +560,13 @@ static int loop_entry(int device, void* stream, int mem, int dtype, int U, int I
                       double* vf_out, int* status, int p_only, void* mu_out = nullptr,
                       void* phi_out = nullptr) {
   reset_launches();
+  // FFCA_MEM_HOST_STATS_DEVICE: host arrays, except the statistics, which stay on the device
+  const bool stats_dev = mem == FFCA_MEM_HOST_STATS_DEVICE;
+  if (stats_dev) mem = FFCA_MEM_HOST;
+  if (mem != FFCA_MEM_HOST && mem != FFCA_MEM_DEVICE) {
+    set_error("bad mem mode %d", mem);
+    return FFCA_E_ARG;
+  }
   if (!check_dims(dtype, U, I, J, N, F)) return FFCA_E_ARG;
   if (I > 8 || J > 8) {
     set_error("unsupported order I=%d / sources J=%d (I <= 8 = matcore.MAX_ORDER, J <= 8)", I, J);
@@ -584,7 +598,8 @@ static int loop_entry(int device, void* stream, int mem, int dtype, int U, int I
 
   // host mode with a large input: pipeline H2D / compute / D2H over chunks
   const size_t in_bytes = size_t(U) * I * N * F * cs + size_t(U) * J * N * F * rs +
-                          (mu_out ? size_t(U) * J * N * F * I * cs : 0) + (phi_out ? size_t(U) * J * N * F * I * rs : 0);
+                          (mu_out && !stats_dev ? size_t(U) * J * N * F * I * cs : 0) +
+                          (phi_out && !stats_dev ? size_t(U) * J * N * F * I * rs : 0);
   // FFCA_NO_PIPELINE=1 disables, FFCA_PIPELINE_MIN_BYTES overrides the threshold (tests)
   const char* nopipe = getenv("FFCA_NO_PIPELINE");
   const char* minb = getenv("FFCA_PIPELINE_MIN_BYTES");
@@ -597,7 +612,7 @@ static int loop_entry(int device, void* stream, int mem, int dtype, int U, int I
     int want = nch_env ? atoi(nch_env) : int(std::min<size_t>(32, std::max<size_t>(2, in_bytes >> 27)));
     const int nchunk = by_mix ? std::min(U, want) : std::min(F, want);
     if (nchunk >= 2) {
-      return pipelined_host_run(device, s, d, record_likelihood != 0, nchunk, by_mix, y, P0, lam0, v0, vf, P_out, lam_out, v_out,
+      return pipelined_host_run(device, s, d, record_likelihood != 0, nchunk, by_mix, stats_dev, y, P0, lam0, v0, vf, P_out, lam_out, v_out,
                                 record_likelihood ? ll_out : nullptr, vf_out, status, mu_out, phi_out);
     }
   }
@@ -615,8 +630,13 @@ static int loop_entry(int device, void* stream, int mem, int dtype, int U, int I
   FFCA_TRY(st.out(v_out, size_t(U) * J * N * F * rs, &ov));
   if (vf_out) FFCA_TRY(st.out(vf_out, size_t(nb) * 8, &ovf));
   if (record_likelihood && ll_out) FFCA_TRY(st.out(ll_out, size_t(U) * nev * 8, &oll));
-  FFCA_TRY(st.out(mu_out, size_t(U) * J * N * F * I * cs, &d.mu));
-  FFCA_TRY(st.out(phi_out, size_t(U) * J * N * F * I * rs, &d.phi));
+  if (stats_dev) {
+    d.mu = mu_out;
+    d.phi = phi_out;
+  } else {
+    FFCA_TRY(st.out(mu_out, size_t(U) * J * N * F * I * cs, &d.mu));
+    FFCA_TRY(st.out(phi_out, size_t(U) * J * N * F * I * rs, &d.phi));
+  }
   void *dstatus, *dllb = nullptr;
   FFCA_TRY(st.scratch(size_t(nb) * 4, &dstatus));
   FFCA_CK(cudaMemsetAsync(dstatus, 0, size_t(nb) * 4, s));

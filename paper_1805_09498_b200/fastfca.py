@@ -72,18 +72,52 @@ class FastFcaParams:
         return FastFcaParams(self.P.copy(), self.Lam.copy(), self.v.copy())
 
 
+class _DeviceArray:
+    """A device-resident array (a torch CUDA tensor) copied to numpy on first host access."""
+
+    __slots__ = ("t",)
+
+    def __init__(self, t):
+        self.t = t
+
+    def numpy(self) -> np.ndarray:
+        return self.t.cpu().numpy()
+
+
 @dataclass
 class TransformedStats:
     """Posterior statistics in the transformed basis (fastfca.py:87-96).
 
     ``mu`` (J, N, F, I) complex holds P^H mu_j and ``phi`` (J, N, F, I) real the
-    diagonal of P^H Phi_j P.  ``run_fastfca`` fills them at the final state in
+    diagonal of P^H Phi_j P.  ``run_fastfca`` computes them at the final state in
     the same device call as the loop (fastfca.py:466), so they are a snapshot:
-    later changes to ``run.params`` do not touch them.
+    later changes to ``run.params`` do not touch them.  The snapshot stays in
+    device memory until a field is first read on the host (then it is copied
+    to numpy once, and from then on is a plain array): a device consumer such
+    as ``wiener.mmse_images_fastfca`` uses it in place, so the statistics
+    never cross PCIe in the reference's estimate -> images flow (cli.py:227-233).
+    ``dataclasses.replace / asdict``, equality and pickling see numpy arrays.
     """
 
     mu: np.ndarray
     phi: np.ndarray
+
+    def __getattribute__(self, name):
+        if name in ("mu", "phi"):
+            d = object.__getattribute__(self, "__dict__")
+            val = d[name]
+            if isinstance(val, _DeviceArray):
+                val = d[name] = val.numpy()
+            return val
+        return object.__getattribute__(self, name)
+
+    def __getstate__(self):
+        return {"mu": self.mu, "phi": self.phi}
+
+    def device_tensor(self, name: str):
+        """The field as a device tensor while it has not been copied to the host, else None."""
+        val = object.__getattribute__(self, "__dict__")[name]
+        return val.t if isinstance(val, _DeviceArray) else None
 
 
 @dataclass
@@ -119,6 +153,14 @@ def _floor_args(v_floor, J, N, F, c64):
         return _lib.VF_BIN, 0.0, _as_r(arr.reshape(F), c64)
     full = np.broadcast_to(arr, (J, N, F))
     return _lib.VF_FULL, 0.0, _as_r(full, c64)
+
+
+def _device_stats_buffers(U, J, N, F, I, c64):
+    """Device tensors for the statistics (U, J, N, F, I) on the library's device."""
+    import torch
+    dev = torch.device("cuda", _lib.device())
+    return (torch.empty((U, J, N, F, I), dtype=torch.complex64 if c64 else torch.complex128, device=dev),
+            torch.empty((U, J, N, F, I), dtype=torch.float32 if c64 else torch.float64, device=dev))
 
 
 def _stats(obs, params, want_mu=True, want_phi=True):
@@ -173,21 +215,22 @@ def run_fastfca(
     P = np.empty_like(P0)
     lam = np.empty_like(lam0)
     v = np.empty_like(v0)
-    mu = np.empty((J, N, F, I), y.dtype)
-    phi = np.empty((J, N, F, I), v0.dtype)
+    mu, phi = _device_stats_buffers(1, J, N, F, I, c64)
     nev = 1 + 2 * int(iterations)
     ll = np.empty((1, nev)) if record_likelihood else None
-    # the loop and the final statistics refresh (fastfca.py:466) in one device call
-    rc = lib.ffca_fastfca_run_stats(_lib.device(), None, _lib.MEM_HOST, code, 1, I, J, N, F,
+    # the loop and the final statistics refresh (fastfca.py:466) in one device call; the
+    # statistics stay in device memory (TransformedStats copies them on first host access)
+    rc = lib.ffca_fastfca_run_stats(_lib.device(), None, _lib.MEM_HOST_STATS_DEVICE, code, 1, I, J, N, F,
                                     _lib.ptr(y), _lib.ptr(P0), _lib.ptr(lam0), _lib.ptr(v0),
                                     mode, vf_scalar, _lib.ptr(vf_arr), int(iterations), int(inner_iterations),
                                     1 if record_likelihood else 0, _lib.ptr(P), _lib.ptr(lam), _lib.ptr(v),
-                                    _lib.ptr(ll), None, None, _lib.ptr(mu), _lib.ptr(phi))
+                                    _lib.ptr(ll), None, None, mu.data_ptr(), phi.data_ptr())
     _lib.check(rc, "ffca_fastfca_run_stats")
     params = FastFcaParams(P=P, Lam=lam, v=v)
     counters = OpCounters()
     counters.add_inversions(int(iterations) * (I + 1) * F * int(inner_iterations))
-    run = FastFcaRun(params=params, stats=TransformedStats(mu=mu, phi=phi), counters=counters)
+    stats = TransformedStats(mu=_DeviceArray(mu[0]), phi=_DeviceArray(phi[0]))
+    run = FastFcaRun(params=params, stats=stats, counters=counters)
     if record_likelihood:
         T = int(iterations)
         run.loglik_init = float(ll[0, 0])
@@ -204,7 +247,9 @@ def run_fastfca_batch(y, P0, lam0, v0, iterations=20, inner_iterations=1, v_floo
     v_floor None (per-mixture power floor) / scalar / (U, F).  Returns
     (P, lam, v, ll (U, 1+2T) or None); with ``stats`` also (mu, phi), each
     (U, J, N, F, I) -- run_fastfca's final refresh for every mixture.  Numpy
-    arrays only.
+    arrays in and out; with ``stats="device"`` the statistics are returned as
+    device (torch) tensors instead and never cross PCIe (``stats_out`` may then
+    be a pair of such tensors to fill).
     """
     y = np.asarray(y)
     if not np.iscomplexobj(y) or y.ndim != 4:
@@ -235,7 +280,17 @@ def run_fastfca_batch(y, P0, lam0, v0, iterations=20, inner_iterations=1, v_floo
     P, lam, v = out if out is not None else (np.empty_like(P0), np.empty_like(lam0), np.empty_like(v0))
     ll = np.empty((U, 1 + 2 * iterations)) if record_likelihood else None
     mu = phi = None
-    if stats:
+    stats_dev = isinstance(stats, str) and stats == "device"
+    if stats_dev:
+        if stats_out is not None:
+            mu, phi = stats_out
+            for o, shape, cplx in ((mu, (U, J, N, F, I), True), (phi, (U, J, N, F, I), False)):
+                if (not hasattr(o, "data_ptr") or not o.is_cuda or tuple(o.shape) != shape or not o.is_contiguous()
+                        or o.is_complex() != cplx or o.element_size() != (y.itemsize if cplx else v0.itemsize)):
+                    raise ValueError(f"stats_out must be contiguous CUDA tensors of shape {shape} in y's precision")
+        else:
+            mu, phi = _device_stats_buffers(U, J, N, F, I, c64)
+    elif stats:
         if stats_out is not None:
             mu, phi = stats_out
             for o, shape, dt in ((mu, (U, J, N, F, I), y.dtype), (phi, (U, J, N, F, I), v0.dtype)):
@@ -245,11 +300,13 @@ def run_fastfca_batch(y, P0, lam0, v0, iterations=20, inner_iterations=1, v_floo
         else:
             mu, phi = np.empty((U, J, N, F, I), y.dtype), np.empty((U, J, N, F, I), v0.dtype)
     lib = _lib.require_gpu()
-    rc = lib.ffca_fastfca_run_stats(_lib.device(), stream, _lib.MEM_HOST, code, U, I, J, N, F,
+    rc = lib.ffca_fastfca_run_stats(_lib.device(), stream, _lib.MEM_HOST_STATS_DEVICE if stats_dev else _lib.MEM_HOST,
+                                    code, U, I, J, N, F,
                                     _lib.ptr(y), _lib.ptr(P0), _lib.ptr(lam0), _lib.ptr(v0), mode, vfs,
                                     _lib.ptr(vfa), iterations, inner_iterations, 1 if record_likelihood else 0,
                                     _lib.ptr(P), _lib.ptr(lam), _lib.ptr(v), _lib.ptr(ll), None, None,
-                                    _lib.ptr(mu), _lib.ptr(phi))
+                                    mu.data_ptr() if stats_dev else _lib.ptr(mu),
+                                    phi.data_ptr() if stats_dev else _lib.ptr(phi))
     _lib.check(rc, "ffca_fastfca_run_stats")
     if stats:
         return P, lam, v, ll, mu, phi
@@ -364,8 +421,28 @@ def log_likelihood(params: FastFcaParams, obs: ObservationTensor) -> float:
     return float(ll[0])
 
 
+def _back_transform_device(P: np.ndarray, mu_t, images_layout: bool) -> np.ndarray:
+    """back_transform_means with mu_tilde already in device memory (a torch CUDA tensor)."""
+    import torch
+    lib = _lib.require_gpu()
+    c64 = mu_t.dtype == torch.complex64
+    J, N, F, I = mu_t.shape
+    P = _as_c(P, c64)
+    if P.shape != (F, I, I):
+        raise DimensionMismatch(f"P must be (F, I, I) = {(F, I, I)}, got {P.shape}")
+    dP = torch.from_numpy(np.ascontiguousarray(P)).to(mu_t.device)
+    out = torch.empty((J, I, N, F) if images_layout else (J, N, F, I), dtype=mu_t.dtype, device=mu_t.device)
+    mu_t = mu_t.contiguous()
+    _lib.check(lib.ffca_back_transform(mu_t.device.index, None, _lib.MEM_DEVICE, _code(c64), 1, I, J, N, F,
+                                       dP.data_ptr(), mu_t.data_ptr(), out.data_ptr(), 1 if images_layout else 0,
+                                       None), "ffca_back_transform")
+    return out.cpu().numpy()
+
+
 def back_transform_means(P: np.ndarray, mu_t: np.ndarray, images_layout: bool = False) -> np.ndarray:
     """Solve P^H mu = mu_tilde per bin; (J, N, F, I) in and out.  fastfca.py:258-273."""
+    if hasattr(mu_t, "is_cuda") and mu_t.is_cuda:
+        return _back_transform_device(P, mu_t, images_layout)
     lib = _lib.require_gpu()
     c64 = np.asarray(mu_t).dtype == np.complex64
     mu_t = _as_c(mu_t, c64)

@@ -37,10 +37,13 @@ def mmse_images_fastfca(params: fastfca.FastFcaParams, stats: fastfca.Transforme
     """Wiener estimates x_j = P^{-H} mu_tilde_j.  wiener.py:38-43.
 
     One device pass: P^{-H} per bin, then the back-solve written straight in
-    the (J, I, N, F) image layout.  (``fastfca.images_from_state`` fuses the
+    the (J, I, N, F) image layout.  Statistics still in device memory (the
+    ``run_fastfca`` snapshot) are used in place; only the images come back.  (``fastfca.images_from_state`` fuses the
     refresh too, for callers that never need mu_tilde.)
     """
-    return SeparatedImages(stft=fastfca.back_transform_means(params.P, stats.mu, images_layout=True))
+    mu_t = stats.device_tensor("mu") if isinstance(stats, fastfca.TransformedStats) else None
+    return SeparatedImages(stft=fastfca.back_transform_means(params.P, stats.mu if mu_t is None else mu_t,
+                                                             images_layout=True))
 
 
 def resynthesize_images(images: SeparatedImages, cfg: StftConfig = StftConfig()) -> SeparatedImages:

@@ -1,9 +1,3 @@
 mkdir -p gpurun_out
-{
-python scripts/fixed_probe.py 4 0
-python scripts/fixed_probe.py 4 20
-python scripts/fixed_probe.py 3 0
-python scripts/fixed_probe.py 3 20
-python scripts/fixed_probe.py 2 0
-python scripts/fixed_probe.py 2 30
-} > gpurun_out/fixed.log 2>&1
+python -m pytest tests -m gpu -x -q > gpurun_out/exp_tests.log 2>&1; echo "pytest rc=$?" >> gpurun_out/exp_tests.log
+timeout 900 python bench.py --no-cpu-baseline --no-extra > gpurun_out/bench_e2e.json 2> gpurun_out/bench_e2e.err; echo "bench rc=$?" >> gpurun_out/exp_tests.log
