@@ -18,6 +18,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
+from ._lazy import DeviceArray, LazyHostFields
 from .errors import DimensionMismatch, NotPositiveDefinite, SingularP
 from .evalkit import OpCounters
 from .stft import ObservationTensor
@@ -72,20 +73,8 @@ class FastFcaParams:
         return FastFcaParams(self.P.copy(), self.Lam.copy(), self.v.copy())
 
 
-class _DeviceArray:
-    """A device-resident array (a torch CUDA tensor) copied to numpy on first host access."""
-
-    __slots__ = ("t",)
-
-    def __init__(self, t):
-        self.t = t
-
-    def numpy(self) -> np.ndarray:
-        return self.t.cpu().numpy()
-
-
 @dataclass
-class TransformedStats:
+class TransformedStats(LazyHostFields):
     """Posterior statistics in the transformed basis (fastfca.py:87-96).
 
     ``mu`` (J, N, F, I) complex holds P^H mu_j and ``phi`` (J, N, F, I) real the
@@ -99,25 +88,9 @@ class TransformedStats:
     ``dataclasses.replace / asdict``, equality and pickling see numpy arrays.
     """
 
+    _LAZY = ("mu", "phi")
     mu: np.ndarray
     phi: np.ndarray
-
-    def __getattribute__(self, name):
-        if name in ("mu", "phi"):
-            d = object.__getattribute__(self, "__dict__")
-            val = d[name]
-            if isinstance(val, _DeviceArray):
-                val = d[name] = val.numpy()
-            return val
-        return object.__getattribute__(self, name)
-
-    def __getstate__(self):
-        return {"mu": self.mu, "phi": self.phi}
-
-    def device_tensor(self, name: str):
-        """The field as a device tensor while it has not been copied to the host, else None."""
-        val = object.__getattribute__(self, "__dict__")[name]
-        return val.t if isinstance(val, _DeviceArray) else None
 
 
 @dataclass
@@ -229,7 +202,7 @@ def run_fastfca(
     params = FastFcaParams(P=P, Lam=lam, v=v)
     counters = OpCounters()
     counters.add_inversions(int(iterations) * (I + 1) * F * int(inner_iterations))
-    stats = TransformedStats(mu=_DeviceArray(mu[0]), phi=_DeviceArray(phi[0]))
+    stats = TransformedStats(mu=DeviceArray(mu[0]), phi=DeviceArray(phi[0]))
     run = FastFcaRun(params=params, stats=stats, counters=counters)
     if record_likelihood:
         T = int(iterations)

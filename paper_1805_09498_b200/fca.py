@@ -15,6 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
+from ._lazy import DeviceArray, LazyHostFields
 from .errors import DimensionMismatch, NotPositiveDefinite
 from .evalkit import OpCounters
 from .stft import ObservationTensor
@@ -68,13 +69,16 @@ class FcaParams:
 
 
 @dataclass
-class PosteriorStats:
+class PosteriorStats(LazyHostFields):
     """Posterior means (J, N, F, I) and covariances (J, N, F, I, I) (fca.py:63-66).
 
     ``run_fca`` returns the last sweep's E-step (at the penultimate parameters,
-    which the loop kernel writes out), computed in the same call.
+    which the loop kernel writes out), computed on the device right after the
+    loop and kept there until a field is first read on the host (then copied to
+    numpy once; see ``_lazy``).
     """
 
+    _LAZY = ("mu", "phi")
     mu: np.ndarray
     phi: np.ndarray
 
@@ -197,20 +201,36 @@ def run_fca(
     if iterations == 0:
         hist = [log_likelihood(init, obs)] if record_likelihood else None
         return FcaRun(params=init, stats=None, counters=counters, loglik=hist)
+    import torch
     lib = _lib.require_gpu()
     c64 = obs.data.dtype == np.complex64
+    code = _code(c64)
     S0, v0 = _as_c(init.S, c64), _as_r(init.v, c64)
     mode, vfs, vfa = _floor_args(v_floor, J, N, F, c64)
-    S, v = np.empty_like(S0), np.empty_like(v0)
-    Sp, vp = np.empty_like(S0), np.empty_like(v0)
-    ll = np.empty((1, 1 + iterations)) if record_likelihood else None
-    _lib.check(lib.ffca_fca_run(_lib.device(), None, _lib.MEM_HOST, _code(c64), 1, I, J, N, F, _lib.ptr(obs.data),
-                                _lib.ptr(S0), _lib.ptr(v0), mode, vfs, _lib.ptr(vfa), int(iterations),
-                                1 if record_likelihood else 0, _lib.ptr(S), _lib.ptr(v), _lib.ptr(Sp), _lib.ptr(vp),
-                                _lib.ptr(ll), None), "ffca_fca_run")
+    # y, the initial state and every result live on the device between the loop and the final
+    # E-step (one H2D of y); S, v (and the likelihood) come back, the statistics stay in HBM
+    dev = torch.device("cuda", _lib.device())
+
+    def up(a):
+        return None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+    dy, dS0, dv0, dvfa = up(obs.data), up(S0), up(v0), up(vfa)
+    dS, dv, dSp, dvp = torch.empty_like(dS0), torch.empty_like(dv0), torch.empty_like(dS0), torch.empty_like(dv0)
+    dll = torch.empty((1, 1 + iterations), dtype=torch.float64, device=dev) if record_likelihood else None
+    ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+    _lib.check(lib.ffca_fca_run(dev.index, None, _lib.MEM_DEVICE, code, 1, I, J, N, F, ptr(dy), ptr(dS0), ptr(dv0),
+                                mode, vfs, ptr(dvfa), int(iterations), 1 if record_likelihood else 0, ptr(dS),
+                                ptr(dv), ptr(dSp), ptr(dvp), ptr(dll), None), "ffca_fca_run")
     counters.add_inversions(iterations * (J + N) * F)
     counters.add_matmuls(iterations * 2 * J * N * F)
-    stats = e_step(FcaParams(Sp, vp), obs)  # fca.py:211: the last sweep's E-step statistics
+    # fca.py:211: the last sweep's E-step statistics, at the penultimate parameters
+    mu = torch.empty((J, N, F, I), dtype=dy.dtype, device=dev)
+    phi = torch.empty((J, N, F, I, I), dtype=dy.dtype, device=dev)
+    _lib.check(lib.ffca_fca_estep(dev.index, None, _lib.MEM_DEVICE, code, 1, I, J, N, F, ptr(dy), ptr(dSp), ptr(dvp),
+                                  ptr(mu), ptr(phi), 0, None), "ffca_fca_estep")
+    stats = PosteriorStats(mu=DeviceArray(mu), phi=DeviceArray(phi))
+    S, v = dS.cpu().numpy(), dv.cpu().numpy()
+    ll = dll.cpu().numpy() if record_likelihood else None
     hist = [float(x) for x in ll[0]] if record_likelihood else None
     return FcaRun(params=FcaParams(S=S, v=v), stats=stats, counters=counters, loglik=hist)
 

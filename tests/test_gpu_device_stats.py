@@ -88,3 +88,19 @@ def test_batch_device_stats_out_validation():
     with pytest.raises(ValueError):
         fastfca.run_fastfca_batch(y[None], P0[None], lam0[None], v0[None], iterations=1, stats="device",
                                   stats_out=bad)
+
+
+@pytest.mark.parametrize("dt", ["c128", "c64"])
+def test_run_fca_statistics_stay_on_device_until_read(dt):
+    from paper_1805_09498_b200 import fca
+    y, _, _, v0, _ = mixture(34, 3, 3, 21, 50)
+    S0 = np.broadcast_to(np.eye(3, dtype=np.complex128), (3, 21, 3, 3)).copy()
+    y, S0, v0 = cast(dt, y, S0, v0)
+    obs = ObservationTensor(y)
+    run = fca.run_fca(obs, fca.FcaParams(S0, v0), iterations=4, record_likelihood=True)
+    assert run.stats.device_tensor("mu") is not None and run.stats.device_tensor("phi") is not None
+    # the statistics are the E-step at the penultimate parameters (fca.py:211)
+    prev = fca.run_fca(obs, fca.FcaParams(S0, v0), iterations=3)
+    ref = fca.e_step(prev.params, obs)
+    assert np.array_equal(run.stats.mu, ref.mu) and np.array_equal(run.stats.phi, ref.phi)
+    assert run.stats.device_tensor("mu") is None and len(run.loglik) == 5
