@@ -426,6 +426,20 @@ def run_ours(args, D):
                                      "traffic -- the kernel holds each bin in shared memory for the whole run"),
         "binding": None,
     }
+    # compute roofline of the same launch: algorithmic FP32 flops of the formulation per TF-point
+    # iteration (phase A: P^H y, |.|^2, weights, d, r2 - r1, v', ratio, s0, s1; phase B: weights,
+    # |y|^2, off-diagonal y y^H, the I accumulations of the I x I B_i) -- per-bin reductions,
+    # reciprocals and the fp64 solves not counted -- against the CUDA-core FP32 peak at the clock
+    # measured during the timed region (148 SMs x 128 lanes x 2 flops)
+    flops_unit = (8 * I * I + 6 * I + 6 * I * J + 7 * J) + (2 * I * J + 3 * I + 3 * I * (I - 1) + 2 * I ** 3)
+    clk_mhz = (clocks or {}).get("sm_mhz") or 1965.0
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    fp_peak = nsm * 128 * 2 * clk_mhz * 1e6 / 1e12
+    fp_ach = flops_unit * units_launch / (k_ms / 1e3) / 1e12
+    roofline["compute"] = {"bound": "fp32 (CUDA cores; no tensor-core work in this path)", "achieved": round(fp_ach, 2),
+                           "peak": round(fp_peak, 2), "unit": "TFLOP/s", "frac": round(fp_ach / fp_peak, 3),
+                           "flops_per_unit": flops_unit,
+                           "peak_source": f"{nsm} SMs x 128 FP32 lanes x 2 x {clk_mhz:.0f} MHz (median SM clock under load)"}
     if prof:
         clk = (clocks or {}).get("sm_mhz") or 1965.0
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
