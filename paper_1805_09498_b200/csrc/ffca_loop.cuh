@@ -235,6 +235,7 @@ __device__ __forceinline__ void bin_reduce_tail(int nv, const T* wpart, double* 
     for (int t = tid; t < G * nv; t += blockDim.x) {
       const int gg = t / nv, k = t % nv;
       double s = 0.0;
+#pragma unroll 8
       for (int r = 0; r < C; ++r) s += cl.map_shared_rank(cp, r)[gg * VMAX + k];
       tot[gg * VMAX + k] = s;
     }
