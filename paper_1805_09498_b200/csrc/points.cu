@@ -142,6 +142,17 @@ __global__ void __launch_bounds__(256) point_kernel(const PointArgs a) {
 // mu_t = g y_t, phi_t = max(v lambda (1 - g), 0)  (fastfca.py:373-387), or the image
 // x_j = Q mu_t written straight into (U, J, I, N, F)  (wiener.py:38-43).
 constexpr int TILE_F = 32, TILE_WARPS = 8;
+// Tile stride along the bins.  With an odd F no 32-bin tile of a row starts on a 32-byte sector,
+// so adjacent tiles would both write (part of) the sector at their boundary -- partial-sector
+// writes the L2 has to merge.  Images tiles therefore overlap by EPS - 1 bins (EPS = elements per
+// 32-byte sector): every sector of a row lies wholly inside some tile, and the tile whose
+// exclusive range [f0, f0 + stride) holds the sector's first bin writes it whole.
+// (complex64 images; measured at config-3 scale 2.10 -> 1.97 ms.  Not for complex128, where a
+// sector holds only two elements: 1.33 -> 1.41 ms.)
+template <typename R, int MODE>
+constexpr int tile_stride() {
+  return (MODE == PM_IMAGES && sizeof(R) == 4) ? TILE_F - (32 / (2 * int(sizeof(R))) - 1) : TILE_F;
+}
 // frames in flight per warp: as many ring stages as fit ~46 KB of static shared memory (<= 4)
 template <typename R, int I>
 constexpr int tile_depth() {
@@ -155,9 +166,12 @@ __global__ void __launch_bounds__(TILE_F* TILE_WARPS, 2) point_tile_kernel(const
   constexpr int JMAX = 4;
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int F = a.F, N = a.N, J = a.J;
-  const int ftiles = (F + TILE_F - 1) / TILE_F;
+  constexpr int TS = tile_stride<R, MODE>();
+  constexpr int EPS = 32 / int(sizeof(C2));  // output elements per 32-byte sector
+  const int ftiles = (F + TS - 1) / TS;
   const long long u = blockIdx.x / ftiles;
-  const int f0 = int(blockIdx.x % ftiles) * TILE_F;
+  const int f0 = int(blockIdx.x % ftiles) * TS;
+  const bool last_tile = f0 + TS >= F;
   const bool live = f0 + lane < F;  // dead lanes of a partial tile compute on a clamped bin, store nothing
   const int f = live ? f0 + lane : F - 1;
   const long long bin = u * F + f;
@@ -293,16 +307,20 @@ __global__ void __launch_bounds__(TILE_F* TILE_WARPS, 2) point_tile_kernel(const
         }
         __syncwarp();
       } else {
-        C2* __restrict__ out = (C2*)a.out0 + (u * J + j) * I * rowN + off;
+        const long long e_row = (u * J + j) * I * rowN + off;  // element index of (j, x = 0, n, f)
+        C2* __restrict__ out = (C2*)a.out0 + e_row;
 #pragma unroll
         for (int x = 0; x < I; ++x) {
+          // first bin of this element's 32-byte sector; the tile owning that bin writes the sector
+          const int b0 = f - int((e_row + x * rowN) & (EPS - 1));
+          const bool own = live && (TS == TILE_F || ((b0 >= f0 || f0 == 0) && (b0 < f0 + TS || last_tile)));
           C2 acc = mk<C2, R>(R(0), R(0));
 #pragma unroll
           for (int b = 0; b < I; ++b) {  // acc += Q[x][b] mu[b] = q.x (mu.x, mu.y) + q.y (-mu.y, mu.x)
             acc = fma2(mu[b], bc2<R>(Qm[x][b].x), acc);
             acc = fma2(mk<C2, R>(-mu[b].y, mu[b].x), bc2<R>(Qm[x][b].y), acc);
           }
-          if (live) out[x * rowN] = acc;
+          if (own) out[x * rowN] = acc;
         }
       }
     }
@@ -387,7 +405,9 @@ int launch_points(int dtype, const PointArgs& a, cudaStream_t s) {
       tf = dtype == FFCA_C64 ? tile_fn<float, PM_STATS>(a.I) : tile_fn<double, PM_STATS>(a.I);
     else
       tf = dtype == FFCA_C64 ? tile_fn<float, PM_IMAGES>(a.I) : tile_fn<double, PM_IMAGES>(a.I);
-    const long long blocks = (long long)a.U * ((a.F + TILE_F - 1) / TILE_F);
+    const int TS = a.mode == PM_IMAGES ? (dtype == FFCA_C64 ? tile_stride<float, PM_IMAGES>() : tile_stride<double, PM_IMAGES>())
+                                       : TILE_F;
+    const long long blocks = (long long)a.U * ((a.F + TS - 1) / TS);
     void* args[] = {(void*)&a};
     FFCA_CK(cudaLaunchKernel(tf, dim3(unsigned(blocks)), dim3(TILE_F * TILE_WARPS), args, 0, s));
     count_launch();
