@@ -157,3 +157,41 @@ def test_cli_device_option_parsing():
     assert Fake.argv == ["bench", "--trials", "2"] and Fake._run_estimator is None
     assert dev_cli.main(["separate", "--device", "cuda", "--iterations", "3"], cli_module=Fake) == 0
     assert Fake.argv == ["separate", "--iterations", "3"] and Fake._run_estimator is dev_cli.run_estimator
+
+
+def test_lazy_statistics_fields_materialise_once():
+    # TransformedStats / PosteriorStats hold device tensors until first read (paper_1805_09498_b200/_lazy.py)
+    import dataclasses
+    import pickle
+
+    from paper_1805_09498_b200._lazy import DeviceArray
+    from paper_1805_09498_b200.fastfca import TransformedStats
+    from paper_1805_09498_b200.fca import PosteriorStats
+
+    class FakeTensor:  # stands in for a CUDA tensor: .cpu().numpy()
+        copies = 0
+
+        def __init__(self, a):
+            self.a = a
+
+        def cpu(self):
+            FakeTensor.copies += 1
+            return self
+
+        def numpy(self):
+            return self.a
+
+    for cls in (TransformedStats, PosteriorStats):
+        FakeTensor.copies = 0
+        mu, phi = np.arange(6.0).reshape(2, 3) + 1j, np.ones((2, 3))
+        st = cls(mu=DeviceArray(FakeTensor(mu)), phi=DeviceArray(FakeTensor(phi)))
+        assert st.device_tensor("mu") is not None and FakeTensor.copies == 0
+        assert np.array_equal(st.mu, mu) and np.array_equal(st.mu, mu) and FakeTensor.copies == 1
+        assert st.device_tensor("mu") is None and st.device_tensor("phi") is not None
+        d = dataclasses.asdict(st)  # reads phi too
+        assert FakeTensor.copies == 2 and np.array_equal(d["phi"], phi)
+        rep = dataclasses.replace(st, phi=np.zeros((2, 3)))
+        assert isinstance(rep.mu, np.ndarray) and not rep.phi.any()
+        back = pickle.loads(pickle.dumps(st))
+        assert np.array_equal(back.mu, mu) and np.array_equal(back.phi, phi)
+        assert [f.name for f in dataclasses.fields(cls)] == ["mu", "phi"]
