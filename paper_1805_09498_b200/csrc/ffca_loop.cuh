@@ -1094,6 +1094,45 @@ __device__ __forceinline__ void invert_P_group(const double2* Pd, double2* Pinv,
     for (int c = 0; c < I; ++c) Pinv[krow * I + c] = er[c];
 }
 
+// [P^-H]_i (i < I <= 4) of every bin of the group from the adjugate of P (cofactors / det),
+// written row-wise into Pinv[(g * I + i) * I + x]; lane t = g * I + i of warp 1 handles bin g,
+// column i.  Flags an exactly singular P (zero determinant) and records log|det P| with rec.
+template <int I, int G>
+__device__ __forceinline__ void pinvh_columns(const double2* Pd, double2* Pinv, double* ldet, int* status,
+                                              long long group, long long total_bins, int crank, bool rec) {
+  if ((threadIdx.x >> 5) != 1) return;
+  const int t = threadIdx.x & 31;
+  const int gg = t / I, i = t % I;
+  const long long b = group * G + gg;
+  const bool act = gg < G && b < total_bins;
+  double2 z[I], det = make_double2(0.0, 0.0);
+  const double2* Pb = Pd + (act ? gg : 0) * I * I;
+  if constexpr (I == 4) {
+    // det along column 0 from the i = 0 lane's cofactors, shuffled to the bin's other lanes
+    adjugate_column<I>(Pb, i, z);
+#pragma unroll
+    for (int x = 0; x < I; ++x) det = cadd(det, cmul(Pb[x * I], z[x]));
+    const int src = (t / I) * I;
+    det.x = __shfl_sync(FULL, det.x, src);
+    det.y = __shfl_sync(FULL, det.y, src);
+  } else {
+    double2 c0[I];
+    adjugate_column<I>(Pb, i, z);
+    adjugate_column<I>(Pb, 0, c0);
+#pragma unroll
+    for (int x = 0; x < I; ++x) det = cadd(det, cmul(Pb[x * I], c0[x]));
+  }
+  if (!act) return;
+  if (det.x == 0.0 && det.y == 0.0 && i == 0 && crank == 0) atomicOr(&status[b], ST_SINGULAR_P);
+  if (rec && i == 0) ldet[gg] = log(hypot(det.x, det.y));
+  const double2 rd = crecip(det);
+#pragma unroll
+  for (int x = 0; x < I; ++x) {  // [P^-H]_{x,i} = conj(P^-1_{i,x}) = conj(C[x][i] / det)
+    const double2 q = cmul(z[x], rd);
+    Pinv[(gg * I + i) * I + x] = make_double2(q.x, -q.y);
+  }
+}
+
 // Slab images for the bulk gather: a 256-thread CTA reads a tile of 32 consecutive bins x FT
 // frames of y (U, I, N, F) and v (U, J, N, F) with bin-contiguous (coalesced) loads into shared
 // memory, then writes each group's records in the loop kernel's slab order -- consecutive lanes
@@ -1378,6 +1417,8 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
   __syncthreads();
 
   const bool rec = !FAST && a.ll != nullptr;
+  // [P^-H] precomputed during the lambda' update (needs a second warp; not in the P-only pass)
+  const bool adj_pre = I <= 4 && blockDim.x >= 64 && (FAST || !a.p_only);
   const bool vf2 = !FAST && a.vf_mode == 2;
   const int KK = FAST ? 1 : a.K;
   const int nev = 1 + 2 * a.iters;
@@ -1482,6 +1523,12 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
           lamd[(gg * J + j) * I + i] = x;
           lamc[(gg * J + j) * I + i] = R(x);
         }
+      }
+      // I <= 4: the columns [P^-H]_i = conj(row i of P^-1) of the current P (from its adjugate) are
+      // formed here by lanes of warp 1 while lanes of warp 0 update lambda -- P does not change
+      // before the solve, so the solve itself starts from them (off the per-iteration chain)
+      if constexpr (I <= 4) {
+        if (adj_pre) pinvh_columns<I, G>(Pd, Pinv, ldet, a.status, group, a.total_bins, crank, rec);
       }
       __syncthreads();
       FFCA_PROBE(2)
@@ -1615,7 +1662,11 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
           // SingularP, as an exactly zero LU pivot does for the structurally singular P the
           // reference rejects (zero rows / columns).
           double2 z[I], det = make_double2(0.0, 0.0);
-          if constexpr (I == 4) {
+          if (k == 0 && adj_pre) {
+            if (bact && s > 0)
+#pragma unroll
+              for (int x = 0; x < I; ++x) z[x] = Pinv[(gg * I + s - 1) * I + x];
+          } else if constexpr (I == 4) {
             // I = 4 (3x3 minors): det along column 0 from the i = 0 thread's own cofactors,
             // shuffled to the bin's other solver threads (lanes of warp 0) -- measured 8.03 ->
             // 7.92 ms at config 2; at I <= 3 recomputing column 0 per thread is faster
@@ -1641,15 +1692,17 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
           FFCA_PROBE(6)
           if (bact && s > 0) {
             const int i = s - 1;
-            if (det.x == 0.0 && det.y == 0.0) {
-              if (i == 0 && crank == 0) atomicOr(&a.status[b], ST_SINGULAR_P);
-            }
-            if (rec && k == 0 && i == 0) ldet[gg] = log(hypot(det.x, det.y));
-            const double2 rd = crecip(det);
+            if (!(k == 0 && adj_pre)) {
+              if (det.x == 0.0 && det.y == 0.0) {
+                if (i == 0 && crank == 0) atomicOr(&a.status[b], ST_SINGULAR_P);
+              }
+              if (rec && k == 0 && i == 0) ldet[gg] = log(hypot(det.x, det.y));
+              const double2 rd = crecip(det);
 #pragma unroll
-            for (int x = 0; x < I; ++x) {  // [P^-H]_{x,i} = conj(P^-1_{i,x}) = conj(C[x][i] / det)
-              const double2 t = cmul(z[x], rd);
-              z[x] = make_double2(t.x, -t.y);
+              for (int x = 0; x < I; ++x) {  // [P^-H]_{x,i} = conj(P^-1_{i,x}) = conj(C[x][i] / det)
+                const double2 t = cmul(z[x], rd);
+                z[x] = make_double2(t.x, -t.y);
+              }
             }
             ldl.solve(z);
 #pragma unroll
