@@ -581,19 +581,40 @@ struct PointWork {
       load_point(yp, vp, yv[0], vj[0]);
       load_point(yp + o1 * RS, vp + o1 * JS, yv[1], vj[1]);
       R q[2][I];
+      {
+        // y_t = P^H y for both frames, row x of P at a time (contiguous in shared memory: vector
+        // loads, every P element read once per frame pair)
+        C2 t0[I], t1[I];
 #pragma unroll
-      for (int b = 0; b < I; ++b) {
-        C2 t0 = mk<C2, R>(R(0), R(0)), t1 = t0;
+        for (int b = 0; b < I; ++b) t0[b] = t1[b] = mk<C2, R>(R(0), R(0));
 #pragma unroll
         for (int x = 0; x < I; ++x) {
-          const C2 pp = P(x, b);
-          t0 = fma2(yv[0][x], bc2<R>(pp.x), t0);
-          t0 = fma2(mk<C2, R>(yv[0][x].y, -yv[0][x].x), bc2<R>(pp.y), t0);
-          t1 = fma2(yv[1][x], bc2<R>(pp.x), t1);
-          t1 = fma2(mk<C2, R>(yv[1][x].y, -yv[1][x].x), bc2<R>(pp.y), t1);
+          C2 prow[I];
+          if constexpr (sizeof(R) == 4 && (I % 2) == 0) {
+#pragma unroll
+            for (int b = 0; b < I; b += 2) {
+              const float4 t = *(const float4*)(Pc + (g * I + x) * I + b);
+              prow[b] = mk<C2, R>(t.x, t.y);
+              prow[b + 1] = mk<C2, R>(t.z, t.w);
+            }
+          } else {
+#pragma unroll
+            for (int b = 0; b < I; ++b) prow[b] = P(x, b);
+          }
+          const C2 s0 = mk<C2, R>(yv[0][x].y, -yv[0][x].x), s1 = mk<C2, R>(yv[1][x].y, -yv[1][x].x);
+#pragma unroll
+          for (int b = 0; b < I; ++b) {
+            t0[b] = fma2(yv[0][x], bc2<R>(prow[b].x), t0[b]);
+            t0[b] = fma2(s0, bc2<R>(prow[b].y), t0[b]);
+            t1[b] = fma2(yv[1][x], bc2<R>(prow[b].x), t1[b]);
+            t1[b] = fma2(s1, bc2<R>(prow[b].y), t1[b]);
+          }
         }
-        q[0][b] = t0.x * t0.x + t0.y * t0.y;
-        q[1][b] = t1.x * t1.x + t1.y * t1.y;
+#pragma unroll
+        for (int b = 0; b < I; ++b) {
+          q[0][b] = t0[b].x * t0[b].x + t0[b].y * t0[b].y;
+          q[1][b] = t1[b].x * t1[b].x + t1[b].y * t1[b].y;
+        }
       }
       R iw[2][I], d[2][I];
 #pragma unroll

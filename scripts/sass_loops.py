@@ -16,7 +16,7 @@ for i, (a, t) in enumerate(ins):
         if ta < a and ta in addr:
             body = [x[1] for x in ins[addr[ta]:i + 1]]
             n = len(body)
-            if n > 400: continue
+            if n > int(sys.argv[2] if len(sys.argv) > 2 else 400): continue
             c = lambda p: sum(1 for b in body if re.search(p, b))
             print(f"loop 0x{ta:x}-0x{a:x}: {n} instr, FP32x2 {c(r'F(FMA|MUL|ADD)2')}, FFMA/FMUL/FADD {c(r'\bF(FMA|MUL|ADD)\b')}, "
                   f"LDS {c(r'LDS')}, STS {c(r'STS')}, MUFU {c(r'MUFU')}, FMNMX {c(r'FMNMX')}, MOV {c(r'\bMOV')}, "
