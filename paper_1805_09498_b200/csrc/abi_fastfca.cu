@@ -88,14 +88,16 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
       if (p.smem <= smem_optin) return FFCA_OK;
     }
   }
-  // complex128, less than one wave of 2-bin CTAs (two per SM): one bin per 128-thread CTA
-  // spreads the bins over more SMs (four such CTAs fit an SM).  Measured: config 0 (513 bins)
+  // complex128: one bin per 128-thread CTA spreads the bins over more SMs (four such CTAs fit an
+  // SM).  Measured: config 0 (513 bins)
   // kernel 0.203 -> 0.197 ms; for complex64 the 4-bin CTAs stay faster (one config-3 mixture
   // 0.109 vs 0.113 ms, two 0.161 vs 0.195 ms), so complex64 keeps G0.
   // The one-bin CTA has half the threads of the G0 = 2 plan -- the same frame slots -- and reduces
   // over 16-lane segments (ffca_loop.cuh bin_reduce), so both plans give bitwise the same bins:
   // results do not depend on the batch size, the host pipeline's chunking or the shard a bin is in.
-  if (dtype == FFCA_C128 && G0 == 2 && I <= 4 && (total_bins + G0 - 1) / G0 < 2LL * nsm) {
+  // Measured on the batched config-3 shape in complex128 as well (256 mixtures): 34.1 ms vs 35.4 ms
+  // for the 2-bin / 256-thread CTAs, so the one-bin CTAs are used at every batch size.
+  if (dtype == FFCA_C128 && G0 == 2 && I <= 4) {
     fill(G0, 1, true);
     const int t2 = p.threads;
     const bool fits2 = p.slab <= kSlabBudget && p.smem <= smem_optin;

@@ -1,5 +1,7 @@
 mkdir -p gpurun_out
 {
-for r in 1 2; do python scripts/exp_time.py 4; done
-} > gpurun_out/exp19.log 2>&1
+DTYPE=c128 python scripts/exp_time.py 3
+python scripts/exp_time.py 0
+python scripts/exp_time.py 4
+} > gpurun_out/exp21.log 2>&1
 python -m pytest tests -m gpu -x -q > gpurun_out/exp_tests.log 2>&1; echo "pytest rc=$?" >> gpurun_out/exp_tests.log

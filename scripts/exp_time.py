@@ -6,6 +6,9 @@ from paper_1805_09498_b200 import _lib
 from paper_1805_09498_b200.workloads import CONFIGS, make_torch
 cid = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 cfg = CONFIGS[cid]
+if os.environ.get("DTYPE"):  # e.g. DTYPE=c128: the same shape in the other precision
+    import dataclasses
+    cfg = dataclasses.replace(cfg, dtype=os.environ["DTYPE"])
 dev = torch.device("cuda", 0)
 lib = _lib.require_gpu()
 U = cfg.mixtures

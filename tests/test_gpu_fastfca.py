@@ -604,16 +604,20 @@ def _plan(dt_code, U, I, J, N, F):
 
 
 def test_c128_results_do_not_depend_on_batch_size():
-    # config-0 shape, complex128: a lone mixture (513 bins, under one wave of 2-bin CTAs) runs
-    # one-bin CTAs, a batch of 4 runs 2-bin CTAs; the one-bin plan reduces over 16-lane
-    # segments so both give bitwise the same bins (the plans used to differ)
+    # config-0 shape, complex128: the default plan runs one-bin CTAs at every batch size; the
+    # 2-bin CTAs (forced here for the batch) must give bitwise the same bins -- the one-bin plan
+    # reduces over 16-lane segments exactly like them (the plans used to differ)
     cfg = CONFIGS[0]
     args = _stack(range(500, 504), cfg.I, cfg.J, cfg.F, cfg.N)
     assert _plan(_lib.C128, 1, 3, 3, cfg.N, cfg.F)[0] == 1
-    assert _plan(_lib.C128, 4, 3, 3, cfg.N, cfg.F)[0] == 2
+    assert _plan(_lib.C128, 4, 3, 3, cfg.N, cfg.F)[0] == 1
     os.environ["FFCA_NO_PIPELINE"] = "1"
     try:
-        batch = fastfca.run_fastfca_batch(*args, iterations=5, record_likelihood=True)
+        os.environ["FFCA_FORCE_PLAN"] = "2,1,1"
+        try:
+            batch = fastfca.run_fastfca_batch(*args, iterations=5, record_likelihood=True)
+        finally:
+            os.environ.pop("FFCA_FORCE_PLAN")
         for u in (0, 3):
             one = fastfca.run_fastfca_batch(*(a[u:u + 1] for a in args), iterations=5, record_likelihood=True)
             for a, b in zip(one, batch):
@@ -623,8 +627,7 @@ def test_c128_results_do_not_depend_on_batch_size():
 
 
 def test_c128_pipelined_chunks_bitwise_one_launch():
-    # 3 config-0 mixtures (69 MB) take the host pipeline in chunks of 2 + 1 mixtures; the 1-mixture
-    # chunk runs the one-bin plan while one launch of all 3 runs 2-bin CTAs
+    # 3 config-0 mixtures (69 MB) take the host pipeline in chunks of 2 + 1 mixtures: bitwise one launch
     cfg = CONFIGS[0]
     args = _stack(range(510, 513), cfg.I, cfg.J, cfg.F, cfg.N)
     os.environ["FFCA_NO_PIPELINE"] = "1"
