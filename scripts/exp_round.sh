@@ -1,7 +1,5 @@
 mkdir -p gpurun_out
 {
-DTYPE=c128 python scripts/exp_time.py 3
-python scripts/exp_time.py 0
-python scripts/exp_time.py 4
-} > gpurun_out/exp21.log 2>&1
-python -m pytest tests -m gpu -x -q > gpurun_out/exp_tests.log 2>&1; echo "pytest rc=$?" >> gpurun_out/exp_tests.log
+python scripts/exp_time.py 2
+for p in 1,4,1,256 1,8,1,256 1,4,1,128 1,16,1,128 1,16,1,64; do echo "plan $p"; FFCA_FORCE_PLAN=$p python scripts/exp_time.py 2; done
+} > gpurun_out/exp22.log 2>&1
