@@ -3,7 +3,10 @@
 This package is a plain-numpy restatement of the reference algorithm
 (``/root/reference/pkg/src/fcasep``) used as the *checker* for the CUDA
 path.  Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
-``cpu_baseline`` / ``--impl reference`` legs may import it.  The product
+``cpu_baseline`` / ``--impl reference`` legs (as the fallback when the stock
+reference is not installed in ``baseline/_ref``) and its after-the-timed-region
+parity check of the timed batch may import it -- always as the checker, never
+as the thing measured.  The product
 package ``paper_1805_09498_b200`` never imports anything from here and has no
 CPU fallback.
 
