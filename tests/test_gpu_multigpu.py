@@ -80,3 +80,47 @@ def test_world2_device_shards_bitwise_unsharded(mode, dt):
             assert np.array_equal(llg, ll)
         else:  # per-F-block partial sums added across ranks: a different summation order
             assert np.allclose(llg, ll, rtol=1e-12 if dt == "c128" else 1e-6, atol=0)
+
+
+def _nccl_worker(port, q):
+    # one rank on the NCCL backend: the collectives the multi-GPU paths issue (all_gather of int64 sizes
+    # and of complex shards viewed as real, all_reduce, gather of padded device buffers) run for real
+    import torch
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        from paper_1805_09498_b200 import _lib
+        from paper_1805_09498_b200.multigpu import run_fastfca_sharded
+
+        _lib.set_device(0)
+        y, P0, lam0, v0 = _inputs("c64")
+        out = run_fastfca_sharded(y, P0, lam0, v0, iterations=3, mode="bins", record_likelihood=True,
+                                  device="cuda:0")
+        # bench.py's Dist.gather_ms pattern: gather a padded device buffer to rank 0
+        src = torch.arange(10, dtype=torch.float32, device="cuda:0")
+        outs = [torch.empty_like(src)]
+        dist.gather(src, outs, dst=0)
+        t = torch.tensor([3.0], dtype=torch.float64, device="cuda:0")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        q.put((out, outs[0].cpu().numpy(), float(t.item()), dist.get_backend()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_backend_world1_collectives():
+    from paper_1805_09498_b200 import fastfca
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(_free_port(), q))
+    p.start()
+    (P, lam, v, ll), g, mx, backend = q.get(timeout=300)
+    p.join(timeout=60)
+    assert p.exitcode == 0 and backend == "nccl"
+    assert np.array_equal(g, np.arange(10, dtype=np.float32)) and mx == 3.0
+    y, P0, lam0, v0 = _inputs("c64")
+    P1, lam1, v1, ll1 = fastfca.run_fastfca_batch(y, P0, lam0, v0, iterations=3, record_likelihood=True)
+    assert np.array_equal(P, P1) and np.array_equal(lam, lam1) and np.array_equal(v, v1)
+    assert np.allclose(ll, ll1, rtol=1e-6, atol=0)
