@@ -14,7 +14,7 @@
 namespace ffca {
 
 using LoopFn = void (*)(const LoopArgs);
-LoopFn loop_kernel_f32(int I, int J, int G, bool res, bool fast);
+LoopFn loop_kernel_f32(int I, int J, int G, bool res, bool fast, bool tm);
 LoopFn loop_kernel_f64(int I, int J, int G, bool res, bool fast);
 
 static bool hot_shape(int I, int J) {
@@ -32,6 +32,7 @@ static int host_vmax(int I, int JM) {
 struct LoopPlan {
   int G = 1, C = 1, NL = 0, threads = 64;
   bool resident = true;
+  bool tm = false;  // y records in tensor memory (ffca_loop.cuh TM)
   size_t smem = 0, slab = 0;
   long long grid = 0;
   LoopSmem L;  // the carve-up the kernel reads from its parameters
@@ -53,7 +54,7 @@ static int choose_threads(int G, int NL, int I) {
 }
 
 static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int vf_mode, LoopPlan& p,
-                     size_t smem_optin, int nsm = 148) {
+                     size_t smem_optin, int nsm = 148, bool fast = false) {
   const int rsz = int(rsize(dtype));
   const int JM = hot_shape(I, J) ? J : 8;
   const int VMAX = host_vmax(I, JM);
@@ -109,6 +110,20 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
       p.smem = L.total;
       if (p.slab <= kSlabBudget && p.smem <= smem_optin) return FFCA_OK;
     }
+  }
+  // complex64, I = J = 3, lean loop, N <= 640: 4-bin CTAs of 128 threads (32 per bin, 10 frame pairs
+  // per thread) with the y records in tensor memory -- 16 bins per SM instead of the 8 that shared
+  // memory alone holds, at the same 16 warps.
+  if (dtype == FFCA_C64 && I == 3 && J == 3 && G0 == 4 && fast && vf_mode != 2 && N <= 640 && getenv("FFCA_TMEM")) {
+    fill(4, 1, true);
+    p.threads = 128;
+    p.tm = true;
+    LoopSmem L(I, J, JM, 4, p.NL, 4, rsz, vf_mode, true, VMAX, true);
+    p.L = L;
+    p.smem = L.total;
+    p.slab = L.slab;
+    if (p.smem <= smem_optin) return FFCA_OK;
+    p.tm = false;
   }
   // complex64, I = J = 3: 2-bin CTAs of 128 threads (64 per bin, as in the 4-bin / 256-thread
   // CTAs) -- four CTAs per SM instead of two overlap each other's reductions and solves better.
@@ -232,8 +247,10 @@ static int launch_problem(int device, const DevProblem& d, cudaStream_t s) {
   if (nb == 0) return FFCA_OK;
   DevAttrs da;
   FFCA_TRY(device_attrs(device, da));
+  // the plain loop (no likelihood, no full floor array, no P-only pass, K = 1) has lean instantiations
+  const bool fast = d.ll_bins == nullptr && d.vf_mode != 2 && !d.p_only && d.K == 1 && !getenv("FFCA_NO_FAST");
   LoopPlan p;
-  FFCA_TRY(plan_loop(d.dtype, d.I, d.J, d.N, nb, d.vf_mode, p, size_t(da.optin), da.nsm));
+  FFCA_TRY(plan_loop(d.dtype, d.I, d.J, d.N, nb, d.vf_mode, p, size_t(da.optin), da.nsm, fast));
   void* scratch = nullptr;
   if (!p.resident) FFCA_CK(cudaMallocAsync(&scratch, size_t(p.grid) * p.slab, s));
   LoopArgs a;
@@ -251,9 +268,7 @@ static int launch_problem(int device, const DevProblem& d, cudaStream_t s) {
   a.slab_bytes = (long long)p.slab;
   a.packed = nullptr;
   a.L = p.L;
-  // the plain loop (no likelihood, no full floor array, no P-only pass, K = 1) has lean instantiations
-  const bool fast = d.ll_bins == nullptr && d.vf_mode != 2 && !d.p_only && d.K == 1 && !getenv("FFCA_NO_FAST");
-  LoopFn fn = d.dtype == FFCA_C64 ? loop_kernel_f32(d.I, d.J, p.G, p.resident, fast)
+  LoopFn fn = d.dtype == FFCA_C64 ? loop_kernel_f32(d.I, d.J, p.G, p.resident, fast, p.tm)
                                   : loop_kernel_f64(d.I, d.J, p.G, p.resident, fast);
   if (!fn) {
     set_error("no kernel for I=%d J=%d", d.I, d.J);

@@ -150,6 +150,42 @@ __device__ __forceinline__ unsigned dynamic_smem_bytes() {
 
 // Asynchronous global -> shared copy of one element (cp.async, LDGSTS);
 // `valid == false` zero-fills the destination without reading the source.
+// ---- tensor memory (TMEM, sm_100a) used as thread-private storage -------------------------
+// 512 columns x 128 lanes x 32 bit per SM.  A CTA allocates a power-of-two number of columns
+// (all 128 lanes); warp w of the CTA reaches lanes 32 (w % 4) .. + 31 only, and the 32x32b
+// shape gives thread t of the warp N consecutive columns of lane 32 (w % 4) + t: a per-thread
+// array that costs neither registers nor shared memory.  Address = (lane << 16) | column.
+template <int COLS>
+__device__ __forceinline__ void tmem_alloc(unsigned* smem_dst) {  // one full warp
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(smem_dst)), "n"(COLS) : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+}
+template <int COLS>
+__device__ __forceinline__ void tmem_dealloc(unsigned taddr) {  // one full warp
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "n"(COLS) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld4(unsigned taddr, float (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+               : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]) : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld8(unsigned taddr, float (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+               : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st4(unsigned taddr, const float (&r)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(taddr), "f"(r[0]), "f"(r[1]),
+               "f"(r[2]), "f"(r[3]) : "memory");
+}
+__device__ __forceinline__ void tmem_st8(unsigned taddr, const float (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(taddr), "f"(r[0]),
+               "f"(r[1]), "f"(r[2]), "f"(r[3]), "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7]) : "memory");
+}
+
 template <int BYTES>
 __device__ __forceinline__ void cp_async(void* smem_dst, const void* gsrc, bool valid) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));

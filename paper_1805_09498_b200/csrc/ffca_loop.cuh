@@ -121,13 +121,13 @@ struct LoopSmem {
   size_t ybytes, vbytes;
   LoopSmem() = default;
   __host__ __device__ LoopSmem(int I, int J, int JM, int G, int NL, int W, int rsz, int vf_mode, bool resident,
-                               int VMAX) {
+                               int VMAX, bool tmem = false) {  // tmem: the y records live in tensor memory
     size_t o = 0;
     const size_t csz = 2 * size_t(rsz);
     const bool ilv = loop_interleaved(I);
     const int JS = loop_js(I, JM, J);
     const size_t NLs = loop_pairs(I, rsz) ? size_t((NL + 1) & ~1) : size_t(NL);  // frame-pair records
-    ybytes = align16(NLs * G * loop_rs(I, JM) * csz);
+    ybytes = tmem ? 0 : align16(NLs * G * loop_rs(I, JM) * csz);
     vbytes = ilv ? 0 : align16(NLs * G * JS * rsz);
     const size_t fs = vf_mode == 2 ? align16(NLs * G * JS * rsz) : 0;
     slab = ybytes + vbytes + fs;
@@ -152,7 +152,7 @@ struct LoopSmem {
     bst = o;   // unused (the solves read the reduced sums in tot)
     {  // solver workspace: per-system matrices (I <= 4) or B_i^-1 + group rows (I > 4)
       const size_t m1 = size_t(G) * (I + 1) * I * I * 16, m2 = (size_t(I) * I * I + 2 * I * (loop_pgroup(I) + 1)) * 16;
-      const int nseg = (G == 1 && !ilv && rsz == 8) ? 2 : 1;  // 16-lane segments (bin_reduce SEG)
+      const int nseg = (G == 1 && !ilv && (rsz == 8 || I == 3)) ? 2 : 1;  // 16-lane segments (bin_reduce SEG)
       size_t wp = align16(size_t(W) * nseg * G * VMAX * rsz);  // warp partials in the compute type
       const size_t ms = align16(m1 > m2 ? m1 : m2);
       if (ilv) {  // I > 4 phase B: per-warp buffers of 32 frames' reciprocal weights
@@ -356,7 +356,7 @@ __device__ __forceinline__ void load_vec(const double* p, double (&o)[N]) {
 }
 
 // Per-point work of one thread over its frames of one bin (registers only).
-template <typename R, int I, int JM, int G>
+template <typename R, int I, int JM, int G, bool TM = false>
 struct PointWork {
   using C2 = typename Cpx<R>::T;
   static constexpr int IC = Shape<I, JM>::IC, NB = Shape<I, JM>::NB, RS = Shape<I, JM>::RS;
@@ -379,6 +379,9 @@ struct PointWork {
   C2 Lp[PREG && !PAIRS ? JM : 1][PREG && !PAIRS ? IP2 : 1];  // lambda as (i, i+1) pairs (FFMA2 over i)
   R Ls[PAIRS ? JM : 1][PAIRS ? I : 1];                        // PAIRS: lambda as scalars (broadcast operands)
   int nfull;  // PAIRS: full frame pairs of this thread
+  unsigned tmy;  // TM: tensor-memory address of this thread's y records (lane quadrant of its warp, column 0)
+  int nrec;      // TM: records per thread (uniform over the CTA: the tcgen05.ld are warp-collective)
+  static constexpr int TMW = 4 * I;  // TM: 32-bit columns per frame-pair record
   bool part;  // PAIRS: this thread also owns the bin's last, half-filled pair (odd frame count)
 
   __device__ __forceinline__ void load_PL() {
@@ -870,15 +873,32 @@ struct PointWork {
   // becomes one packed FFMA2 for both frames; sums over frames are kept as (even, odd) pairs and
   // added at the end.  PART: frame b is the zero padding after an odd frame count -- its power
   // stays 0 and it contributes nothing (its floor is replaced by 1 so 0 / v' is 0, never 0 / 0).
-  __device__ __forceinline__ void load_pair(const C2* yp, const R* vp, C2 (&ya)[I], C2 (&yb)[I], C2 (&v2)[JM]) const {
+  __device__ __forceinline__ void load_y_pair(const C2* yp, C2 (&ya)[I], C2 (&yb)[I]) const {
 #pragma unroll
     for (int i = 0; i < I; ++i) {
       const float4 t = *(const float4*)(yp + 2 * i);
       ya[i] = mk<C2, R>(t.x, t.y);
       yb[i] = mk<C2, R>(t.z, t.w);
     }
+  }
+  __device__ __forceinline__ void load_v_pair(const R* vp, C2 (&v2)[JM]) const {
 #pragma unroll
     for (int j = 0; j < JM; ++j) v2[j] = (j < J) ? *(const C2*)(vp + 2 * j) : mk<C2, R>(R(0), R(0));
+  }
+  __device__ __forceinline__ void load_pair(const C2* yp, const R* vp, C2 (&ya)[I], C2 (&yb)[I], C2 (&v2)[JM]) const {
+    load_y_pair(yp, ya, yb);
+    load_v_pair(vp, v2);
+  }
+  // TM: record k of this thread from tensor memory (warp-collective: every lane of the warp calls it)
+  __device__ __forceinline__ void tm_load_pair(int k, C2 (&ya)[I], C2 (&yb)[I]) const {
+    static_assert(!TM || (I == 3 && sizeof(R) == 4), "tensor-memory records: complex64, I = 3");
+    float r8[8], r4[4];
+    tmem_ld8(tmy + k * TMW, r8);
+    tmem_ld4(tmy + k * TMW + 8, r4);
+    tmem_wait_ld();
+    ya[0] = mk<C2, R>(r8[0], r8[1]); yb[0] = mk<C2, R>(r8[2], r8[3]);
+    ya[1] = mk<C2, R>(r8[4], r8[5]); yb[1] = mk<C2, R>(r8[6], r8[7]);
+    ya[2] = mk<C2, R>(r4[0], r4[1]); yb[2] = mk<C2, R>(r4[2], r4[3]);
   }
   // q_b = |(P^H y)_b|^2 for both frames, as a pair
   __device__ __forceinline__ void q_pair(const C2 (&ya)[I], const C2 (&yb)[I], C2 (&q2)[I]) const {
@@ -913,8 +933,15 @@ struct PointWork {
   template <bool REC, bool VF2, bool PART>
   __device__ __forceinline__ void pairA(const C2* yp, R* vp, const R* fp, C2 (&s0)[JM], C2 (&s1)[JM][I], C2& lacc,
                                         const R vfl_b) const {
-    C2 ya[I], yb[I], v2[JM];
-    load_pair(yp, vp, ya, yb, v2);
+    C2 ya[I], yb[I];
+    load_y_pair(yp, ya, yb);
+    pairA_core<REC, VF2, PART>(ya, yb, vp, fp, s0, s1, lacc, vfl_b);
+  }
+  template <bool REC, bool VF2, bool PART>
+  __device__ __forceinline__ void pairA_core(const C2 (&ya)[I], const C2 (&yb)[I], R* vp, const R* fp, C2 (&s0)[JM],
+                                             C2 (&s1)[JM][I], C2& lacc, const R vfl_b) const {
+    C2 v2[JM];
+    load_v_pair(vp, v2);
     C2 q2[I], iw2[I], w2[I], d2[I];
     q_pair(ya, yb, q2);
     iw_pair(v2, iw2, w2);
@@ -964,9 +991,19 @@ struct PointWork {
     R* vp = vs + rec0 * 2 * JS;
     const R* fp = vfs + rec0 * 2 * JS;
     const int sy = rstep * 2 * RS, sv = rstep * 2 * JS;
+    if constexpr (TM) {
+#pragma unroll 1
+      for (int k = 0; k < nrec; ++k, vp += sv, fp += sv) {
+        C2 ya[I], yb[I];
+        tm_load_pair(k, ya, yb);
+        if (k < nfull) pairA_core<REC, VF2, false>(ya, yb, vp, fp, s0, s1, lacc, vfl_b);
+        else if (part && k == nfull) pairA_core<REC, VF2, true>(ya, yb, vp, fp, s0, s1, lacc, vfl_b);
+      }
+    } else {
 #pragma unroll 1
     for (int k = 0; k < nfull; ++k, yp += sy, vp += sv, fp += sv) pairA<REC, VF2, false>(yp, vp, fp, s0, s1, lacc, vfl_b);
     if (part) pairA<REC, VF2, true>(yp, vp, fp, s0, s1, lacc, vfl_b);
+    }
 #pragma unroll
     for (int j = 0; j < JM; ++j) {
       acc[j] = s0[j].x + s0[j].y;
@@ -978,8 +1015,15 @@ struct PointWork {
 
   template <bool REC, bool PART>
   __device__ __forceinline__ void pairB(const C2* yp, const R* vp, C2 (&ac)[I][NCXP], C2 (&ad)[I][I], C2& lacc) const {
-    C2 ya[I], yb[I], v2[JM];
-    load_pair(yp, vp, ya, yb, v2);
+    C2 ya[I], yb[I];
+    load_y_pair(yp, ya, yb);
+    pairB_core<REC, PART>(ya, yb, vp, ac, ad, lacc);
+  }
+  template <bool REC, bool PART>
+  __device__ __forceinline__ void pairB_core(const C2 (&ya)[I], const C2 (&yb)[I], const R* vp, C2 (&ac)[I][NCXP],
+                                             C2 (&ad)[I][I], C2& lacc) const {
+    C2 v2[JM];
+    load_v_pair(vp, v2);
     C2 iw2[I], w2[I];
     iw_pair(v2, iw2, w2);
     if constexpr (REC) {
@@ -1033,9 +1077,19 @@ struct PointWork {
     const C2* yp = ys + rec0 * 2 * RS;
     const R* vp = vs + rec0 * 2 * JS;
     const int sy = rstep * 2 * RS, sv = rstep * 2 * JS;
+    if constexpr (TM) {
+#pragma unroll 1
+      for (int k = 0; k < nrec; ++k, vp += sv) {
+        C2 ya[I], yb[I];
+        tm_load_pair(k, ya, yb);
+        if (k < nfull) pairB_core<REC, false>(ya, yb, vp, ac, ad, lacc);
+        else if (part && k == nfull) pairB_core<REC, true>(ya, yb, vp, ac, ad, lacc);
+      }
+    } else {
 #pragma unroll 1
     for (int k = 0; k < nfull; ++k, yp += sy, vp += sv) pairB<REC, false>(yp, vp, ac, ad, lacc);
     if (part) pairB<REC, true>(yp, vp, ac, ad, lacc);
+    }
 #pragma unroll
     for (int i = 0; i < I; ++i) {
       R* o = acc + i * I * I;
@@ -1240,8 +1294,9 @@ __global__ void __launch_bounds__(256) slab_pack_kernel(const PackArgs a) {
 // FAST: the plain estimation loop (no likelihood recording, no full floor array, no P-only pass,
 // one inner iteration) -- those paths compile out, which keeps the hot instantiations smaller
 // (instruction cache) and lighter on registers.  The launcher picks it when a call allows.
-template <typename R, int I, int JT, int G, bool RES, bool FAST = false>
-__global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffca_loop_kernel(const LoopArgs a) {
+template <typename R, int I, int JT, int G, bool RES, bool FAST = false, bool TM = false>
+__global__ void __launch_bounds__(TM ? 128 : 256, TM ? 4 : ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffca_loop_kernel(const LoopArgs a) {
+  static_assert(!TM || (FAST && RES && G == 4 && I == 3 && sizeof(R) == 4), "tensor-memory plan: the lean complex64 I = 3 loop");
   using C2 = typename Cpx<R>::T;
   constexpr int JM = JT > 0 ? JT : 8;
   constexpr int IC = Shape<I, JM>::IC, NCH = Shape<I, JM>::NCH, NB = Shape<I, JM>::NB;
@@ -1256,7 +1311,7 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
   const int g = tid % G;
   const int slot = tid / G, nslots = blockDim.x / G;
   // complex128 one-bin CTAs reduce over 16-lane segments (bin_reduce): bitwise the G = 2 plan
-  constexpr int SEG = (G == 1 && I <= 4 && sizeof(R) == 8) ? 16 : 32 / G;
+  constexpr int SEG = (G == 1 && I <= 4 && (sizeof(R) == 8 || I == 3)) ? 16 : 32 / G;
   constexpr bool PAIRS = loop_pairs(I, int(sizeof(R)));
 
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1310,6 +1365,40 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
   // filled with cp.async (zero-fill for padding), keeping every load of the
   // thread in flight at once.
   __shared__ unsigned long long gather_bar;
+  // TM: the y records of the CTA's bins live in tensor memory as thread-private arrays (thread t
+  // owns frame pairs slot + k nslots, k < nrec, 4 I columns each): 128 columns x 128 lanes per CTA,
+  // four CTAs fill the SM's 512 columns.  Shared memory holds only the powers v.
+  __shared__ unsigned tm_base_s;
+  constexpr int TMCOLS = 128;
+  unsigned tmy = 0;
+  const int nrec = (NLs / 2 + nslots - 1) / nslots;
+  if constexpr (TM) {
+    if (nrec * 4 * I > TMCOLS || blockDim.x != 128) __trap();
+    if (tid < 32) tmem_alloc<TMCOLS>(&tm_base_s);
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    tmy = tm_base_s + ((unsigned((tid >> 5) & 3) * 32u) << 16);
+#pragma unroll 2
+    for (int k = 0; k < nrec; ++k) {
+      const int m = slot + k * nslots;
+      float r8[8], r4[4];
+#pragma unroll
+      for (int i = 0; i < I; ++i)
+#pragma unroll
+        for (int par = 0; par < 2; ++par) {
+          const int n = 2 * m + par;
+          C2 z = mk<C2, R>(R(0), R(0));
+          if (active && n < NLr) z = __ldg(yg + ((u * I + i) * (long long)N + n0 + n) * F + f);
+          const int w = 4 * i + 2 * par;
+          if (w < 8) { r8[w] = z.x; r8[w + 1] = z.y; }
+          else { r4[w - 8] = z.x; r4[w - 7] = z.y; }
+        }
+      tmem_st8(tmy + k * 4 * I, r8);
+      tmem_st4(tmy + k * 4 * I + 8, r4);
+    }
+    tmem_wait_st();
+  }
   if (a.packed && resident) {
     // one TMA-engine bulk copy stream of this CTA's contiguous slab image (y and v records)
     const unsigned bytes = unsigned(L.ybytes + L.vbytes);
@@ -1333,7 +1422,7 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
       const long long gstep = (long long)nslots * F;
       const int ystep = nslots * G * RS, vstep = nslots * G * JS;
 #pragma unroll 1
-      for (int i = 0; i < I; ++i) {
+      for (int i = 0; i < (TM ? 0 : I); ++i) {
         const C2* col = yg + ((u * I + i) * (long long)N + n0) * F + f;
         const C2* src = col + (long long)slot * F;
         C2* dst = ys + slab_y<PAIRS>(slot, g, i, G, RS);
@@ -1413,7 +1502,18 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
   // ---------------- v floor per bin (fca.py:82-89 when auto) ----------------
   if (a.vf_mode == 3) {
     R psum = R(0);
-    if (active)
+    if constexpr (TM) {  // own records (zero padding adds nothing); warp-collective loads
+      for (int k = 0; k < nrec; ++k) {
+        float r8[8], r4[4];
+        tmem_ld8(tmy + k * 4 * I, r8);
+        tmem_ld4(tmy + k * 4 * I + 8, r4);
+        tmem_wait_ld();
+#pragma unroll
+        for (int w = 0; w < 8; ++w) psum = fma(R(r8[w]), R(r8[w]), psum);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) psum = fma(R(r4[w]), R(r4[w]), psum);
+      }
+    } else if (active)
       for (int n = slot; n < NLr; n += nslots)
 #pragma unroll
         for (int i = 0; i < I; ++i) {
@@ -1450,7 +1550,8 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
   const int rstep = nslots * G;           // records between a thread's frames (= blockDim.x)
   const int npts = active ? (NLr > slot ? (NLr - slot + nslots - 1) / nslots : 0) : 0;
 
-  PointWork<R, I, JM, G> pw;
+  PointWork<R, I, JM, G, TM> pw;
+  pw.tmy = tmy; pw.nrec = nrec;
   pw.ys = ys; pw.vs = vs; pw.vfs = vfs; pw.Pc = Pc; pw.lamc = lamc;
   pw.gslab = !resident;
   pw.g = g; pw.J = J; pw.JS = JS; pw.rec0 = rec0; pw.rstep = rstep; pw.npts = npts;
@@ -1851,6 +1952,11 @@ __global__ void __launch_bounds__(256, ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffc
     }
   }
   FFCA_FIXED(2)
+  if constexpr (TM) {
+    tmem_fence_before();
+    __syncthreads();
+    if (tid < 32) tmem_dealloc<TMCOLS>(tm_base_s);
+  }
   // no CTA may exit while a peer can still read its shared memory
   if (C > 1) cg::this_cluster().sync();
 }

@@ -9,24 +9,29 @@ using LoopFn = void (*)(const LoopArgs);
 // sector of float complex) when a bin fits one CTA, G = 1 for clusters / the
 // global-slab path.
 template <int I, int J>
-static LoopFn hot(int G, bool res, bool fast) {
+static LoopFn hot(int G, bool res, bool fast, bool tm) {
+  if constexpr (I == 3 && J == 3)
+    if (tm) return (G == 4 && res && fast) ? (LoopFn)ffca_loop_kernel<float, 3, 3, 4, true, true, true> : nullptr;
   if constexpr (I <= 4) {
+    if constexpr (I == 3 && J == 3)
+      if (G == 4 && res && fast) return ffca_loop_kernel<float, I, J, 4, true, true>;
     if (G == 4 && res) return ffca_loop_kernel<float, I, J, 4, true>;
     if constexpr (I == 3 && J == 3)
       if (G == 2 && res)
         return fast ? (LoopFn)ffca_loop_kernel<float, I, J, 2, true, true> : (LoopFn)ffca_loop_kernel<float, I, J, 2, true>;
   }
-  if constexpr ((I == 4 && J == 4) || (I == 8 && J == 6))  // the config-2 / config-4 cluster plans
+  if constexpr ((I == 4 && J == 4) || (I == 8 && J == 6) || (I == 3 && J == 3))  // the config-2 / config-4 cluster plans, one-bin config 3
     if (G == 1 && res && fast) return ffca_loop_kernel<float, I, J, 1, true, true>;
   if (G == 1) return res ? (LoopFn)ffca_loop_kernel<float, I, J, 1, true> : (LoopFn)ffca_loop_kernel<float, I, J, 1, false>;
   return nullptr;
 }
 
-LoopFn loop_kernel_f32(int I, int J, int G, bool res, bool fast) {
-  if (I == 3 && J == 3) return hot<3, 3>(G, res, fast);
-  if (I == 4 && J == 4) return hot<4, 4>(G, res, fast);
-  if (I == 8 && J == 6) return hot<8, 6>(G, res, fast);
-  if (I == 2 && J == 2) return hot<2, 2>(G, res, false);
+LoopFn loop_kernel_f32(int I, int J, int G, bool res, bool fast, bool tm) {
+  if (tm && !(I == 3 && J == 3)) return nullptr;
+  if (I == 3 && J == 3) return hot<3, 3>(G, res, fast, tm);
+  if (I == 4 && J == 4) return hot<4, 4>(G, res, fast, false);
+  if (I == 8 && J == 6) return hot<8, 6>(G, res, fast, false);
+  if (I == 2 && J == 2) return hot<2, 2>(G, res, false, false);
   if (J > 8 || G != 1) return nullptr;
   // runtime J (<= 8); residency decided at run time (scratch == nullptr) -- except the resident
   // I > 4 plans, which run one CTA per SM and get the 255-register instantiation
