@@ -340,12 +340,13 @@ def device_runner(lib, _lib, code, dev, stream, y, P0, lam0, v0, T):
 
 
 def plan_name(lib, _lib, code, U, I, J, N, F):
-    out = np.zeros(6, np.int32)
-    lib.ffca_plan_loop(0, code, U, I, J, N, F, _lib.VF_AUTO, out.ctypes.data_as(_lib._ip))
-    G, C, NL, thr, res, smem = (int(x) for x in out)
+    out = np.zeros(8, np.int32)
+    lib.ffca_plan_loop_ex(0, code, U, I, J, N, F, _lib.VF_AUTO, 1, out.ctypes.data_as(_lib._ip))
+    G, C, NL, thr, res, smem, tm, tmcols = (int(x) for x in out)
     R = "float" if code == _lib.C64 else "double"
-    return f"ffca_loop_kernel<{R},{I},{J},{G},{str(bool(res)).lower()}>", {
-        "G": G, "cluster": C, "frames_per_cta": NL, "threads": thr, "resident": bool(res), "smem_bytes": smem}
+    name = f"ffca_loop_kernel<{R},{I},{J},{G},{str(bool(res)).lower()}" + (",true,true>" if tm else ">")
+    return name, {"G": G, "cluster": C, "frames_per_cta": NL, "threads": thr, "resident": bool(res),
+                  "smem_bytes": smem, "y_records_in_tensor_memory": bool(tm), "tmem_columns_per_cta": tmcols}
 
 
 def parity_check(y, P0, lam0, v0, outs, T, picks):

@@ -243,6 +243,10 @@ int ffca_stft_synthesize(int device, void* stream, int mem, int dtype, int I, in
 
 /* Launch plan of the loop kernel for a shape: out6 = {G, C, NL, threads, resident, smem}. */
 int ffca_plan_loop(int device, int dtype, int U, int I, int J, int N, int F, int vf_mode, int* out6);
+/* Same with the loop variant chosen (lean != 0: the plain loop; 0: likelihood record / inner
+ * iterations) and the tensor-memory use: out8 = {G, C, NL, threads, resident, smem, tensor-memory
+ * plan (y records in TMEM), TMEM columns per CTA}. */
+int ffca_plan_loop_ex(int device, int dtype, int U, int I, int J, int N, int F, int vf_mode, int lean, int* out8);
 
 /* Kernel launches issued by the last successful call on this host thread. */
 int ffca_last_launch_count(void);

@@ -47,6 +47,7 @@ SIGNATURES = {
     "ffca_set_kernel_timing": [_i],
     "ffca_last_kernel_ms": [],
     "ffca_plan_loop": [_i, _i, _i, _i, _i, _i, _i, _i, _ip],
+    "ffca_plan_loop_ex": [_i, _i, _i, _i, _i, _i, _i, _i, _i, _ip],
     "ffca_fastfca_run": [_i, _vp, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _i, _d, _vp, _i, _i, _i,
                          _vp, _vp, _vp, _vp, _vp, _vp],
     "ffca_fastfca_run_stats": [_i, _vp, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _i, _d, _vp, _i, _i, _i,

@@ -114,7 +114,7 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
   // complex64, I = J = 3, lean loop, N <= 640: 4-bin CTAs of 128 threads (32 per bin, 10 frame pairs
   // per thread) with the y records in tensor memory -- 16 bins per SM instead of the 8 that shared
   // memory alone holds, at the same 16 warps.
-  if (dtype == FFCA_C64 && I == 3 && J == 3 && G0 == 4 && fast && vf_mode != 2 && N <= 640 && getenv("FFCA_TMEM")) {
+  if (dtype == FFCA_C64 && I == 3 && J == 3 && G0 == 4 && fast && vf_mode != 2 && N <= 640 && !getenv("FFCA_NO_TMEM")) {
     fill(4, 1, true);
     p.threads = 128;
     p.tm = true;
@@ -781,8 +781,8 @@ extern "C" int ffca_fixed_point_update_P(int device, void* stream, int mem, int 
 }
 
 // Introspection for tests / bench: the launch plan chosen for a shape.
-extern "C" int ffca_plan_loop(int device, int dtype, int U, int I, int J, int N, int F, int vf_mode,
-                              int* out6) {
+static int plan_introspect(int device, int dtype, int U, int I, int J, int N, int F, int vf_mode, bool fast,
+                           LoopPlan& p) {
   int optin = 0;
   if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) != cudaSuccess) {
     cudaGetLastError();
@@ -793,13 +793,36 @@ extern "C" int ffca_plan_loop(int device, int dtype, int U, int I, int J, int N,
     cudaGetLastError();
     nsm = 148;
   }
+  return plan_loop(dtype, I, J, N, (long long)U * F, vf_mode, p, size_t(optin), nsm, fast);
+}
+
+// The plan of the plain loop (no likelihood record, K = 1: the lean instantiations).
+extern "C" int ffca_plan_loop(int device, int dtype, int U, int I, int J, int N, int F, int vf_mode,
+                              int* out6) {
   LoopPlan p;
-  int rc = plan_loop(dtype, I, J, N, (long long)U * F, vf_mode, p, size_t(optin), nsm);
+  int rc = plan_introspect(device, dtype, U, I, J, N, F, vf_mode, vf_mode != 2 && !getenv("FFCA_NO_FAST"), p);
   out6[0] = p.G;
   out6[1] = p.C;
   out6[2] = p.NL;
   out6[3] = p.threads;
   out6[4] = p.resident ? 1 : 0;
   out6[5] = int(p.smem);
+  return rc;
+}
+
+// lean != 0: the plain loop; lean == 0: the loop with the likelihood record / inner iterations.
+// out8 = {G, C, NL, threads, resident, smem, tensor-memory plan, tensor-memory columns per CTA}.
+extern "C" int ffca_plan_loop_ex(int device, int dtype, int U, int I, int J, int N, int F, int vf_mode, int lean,
+                                 int* out8) {
+  LoopPlan p;
+  int rc = plan_introspect(device, dtype, U, I, J, N, F, vf_mode, lean != 0 && vf_mode != 2 && !getenv("FFCA_NO_FAST"), p);
+  out8[0] = p.G;
+  out8[1] = p.C;
+  out8[2] = p.NL;
+  out8[3] = p.threads;
+  out8[4] = p.resident ? 1 : 0;
+  out8[5] = int(p.smem);
+  out8[6] = p.tm ? 1 : 0;
+  out8[7] = p.tm ? 128 : 0;
   return rc;
 }

@@ -167,6 +167,15 @@ __device__ __forceinline__ void tmem_dealloc(unsigned taddr) {  // one full warp
 __device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+// wait::ld that also "touches" the destination registers of the loads it completes, so the
+// compiler cannot schedule a use of them before the wait
+__device__ __forceinline__ void tmem_wait_ld(float (&a)[8], float (&b)[4]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+f"(a[0]), "+f"(a[1]), "+f"(a[2]), "+f"(a[3]), "+f"(a[4]), "+f"(a[5]), "+f"(a[6]), "+f"(a[7]), "+f"(b[0]),
+                 "+f"(b[1]), "+f"(b[2]), "+f"(b[3])
+               :
+               : "memory");
+}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void tmem_ld4(unsigned taddr, float (&r)[4]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"

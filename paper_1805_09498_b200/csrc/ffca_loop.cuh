@@ -895,7 +895,7 @@ struct PointWork {
     float r8[8], r4[4];
     tmem_ld8(tmy + k * TMW, r8);
     tmem_ld4(tmy + k * TMW + 8, r4);
-    tmem_wait_ld();
+    tmem_wait_ld(r8, r4);
     ya[0] = mk<C2, R>(r8[0], r8[1]); yb[0] = mk<C2, R>(r8[2], r8[3]);
     ya[1] = mk<C2, R>(r8[4], r8[5]); yb[1] = mk<C2, R>(r8[6], r8[7]);
     ya[2] = mk<C2, R>(r4[0], r4[1]); yb[2] = mk<C2, R>(r4[2], r4[3]);
@@ -1507,7 +1507,7 @@ __global__ void __launch_bounds__(TM ? 128 : 256, TM ? 4 : ((I == 4 || (I > 4 &&
         float r8[8], r4[4];
         tmem_ld8(tmy + k * 4 * I, r8);
         tmem_ld4(tmy + k * 4 * I + 8, r4);
-        tmem_wait_ld();
+        tmem_wait_ld(r8, r4);
 #pragma unroll
         for (int w = 0; w < 8; ++w) psum = fma(R(r8[w]), R(r8[w]), psum);
 #pragma unroll

@@ -52,9 +52,19 @@ def test_plan_introspection_without_device():
     from paper_1805_09498_b200 import _lib
     lib = _lib.load()
     out = np.zeros(6, np.int32)
-    # config 3 shape (c64, I=J=3, N=626): 2 lane-interleaved bins per 128-thread CTA, resident
+    # config 3 shape (c64, I=J=3, N=626), plain loop: 4 lane-interleaved bins per 128-thread CTA with the
+    # y records in tensor memory (128 columns per CTA; shared memory holds only the powers)
+    out8 = np.zeros(8, np.int32)
     assert lib.ffca_plan_loop(0, _lib.C64, 256, 3, 3, 626, 513, _lib.VF_AUTO, out.ctypes.data_as(_lib._ip)) == 0
-    assert out[0] == 2 and out[1] == 1 and out[3] == 128 and out[4] == 1
+    assert out[0] == 4 and out[1] == 1 and out[3] == 128 and out[4] == 1 and out[5] < 48 * 1024
+    assert lib.ffca_plan_loop_ex(0, _lib.C64, 256, 3, 3, 626, 513, _lib.VF_AUTO, 1, out8.ctypes.data_as(_lib._ip)) == 0
+    assert list(out8[:6]) == list(out) and out8[6] == 1 and out8[7] == 128
+    # ... the loop with the likelihood record keeps 2 bins per 128-thread CTA in shared memory
+    assert lib.ffca_plan_loop_ex(0, _lib.C64, 256, 3, 3, 626, 513, _lib.VF_AUTO, 0, out8.ctypes.data_as(_lib._ip)) == 0
+    assert out8[0] == 2 and out8[3] == 128 and out8[4] == 1 and out8[6] == 0
+    # ... and so do bins longer than the 640 frames a CTA's 128 columns hold
+    assert lib.ffca_plan_loop_ex(0, _lib.C64, 256, 3, 3, 642, 513, _lib.VF_AUTO, 1, out8.ctypes.data_as(_lib._ip)) == 0
+    assert out8[0] == 2 and out8[6] == 0
     # other complex64 hot shapes keep 4 lane-interleaved bins
     assert lib.ffca_plan_loop(0, _lib.C64, 64, 2, 2, 626, 513, _lib.VF_AUTO, out.ctypes.data_as(_lib._ip)) == 0
     assert out[0] == 4
