@@ -162,6 +162,24 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
   }
   for (int C = 2; C <= 8; C <<= 1) {
     if (C > N) break;
+    // complex64, I = J = 4, lean loop: with the y records in tensor memory (256 columns per CTA, two
+    // CTAs per SM) a CTA holds up to 4096 frames, so a long bin needs a smaller cluster than shared
+    // memory alone allows (config 2: 4 CTAs per bin instead of 8 -- half the DSMEM reduction ranks)
+    if (dtype == FFCA_C64 && I == 4 && J == 4 && hot_shape(I, J) && fast && vf_mode != 2 && !getenv("FFCA_NO_TMEM")) {
+      const int NLc = (N + C - 1) / C;
+      const int nrec = ((NLc + 1) / 2 + 127) / 128;
+      if (nrec * 16 <= 256) {
+        fill(1, C, true);
+        p.threads = 128;
+        p.tm = true;
+        LoopSmem L(I, J, JM, 1, p.NL, 4, rsz, vf_mode, true, VMAX, true);
+        p.L = L;
+        p.smem = L.total;
+        p.slab = L.slab;
+        if (p.slab <= kSlabBudget && p.smem <= smem_optin) return FFCA_OK;
+        p.tm = false;
+      }
+    }
     fill(1, C, true);
     if (p.slab <= kSlabBudget && p.smem <= smem_optin) return FFCA_OK;
   }
@@ -823,6 +841,6 @@ extern "C" int ffca_plan_loop_ex(int device, int dtype, int U, int I, int J, int
   out8[4] = p.resident ? 1 : 0;
   out8[5] = int(p.smem);
   out8[6] = p.tm ? 1 : 0;
-  out8[7] = p.tm ? 128 : 0;
+  out8[7] = p.tm ? (I == 3 ? 128 : 256) : 0;
   return rc;
 }

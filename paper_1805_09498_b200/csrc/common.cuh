@@ -155,14 +155,12 @@ __device__ __forceinline__ unsigned dynamic_smem_bytes() {
 // (all 128 lanes); warp w of the CTA reaches lanes 32 (w % 4) .. + 31 only, and the 32x32b
 // shape gives thread t of the warp N consecutive columns of lane 32 (w % 4) + t: a per-thread
 // array that costs neither registers nor shared memory.  Address = (lane << 16) | column.
-template <int COLS>
-__device__ __forceinline__ void tmem_alloc(unsigned* smem_dst) {  // one full warp
-  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(smem_dst)), "n"(COLS) : "memory");
+__device__ __forceinline__ void tmem_alloc(unsigned* smem_dst, unsigned cols) {  // one full warp; cols = 32 .. 512, power of 2
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(smem_dst)), "r"(cols) : "memory");
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
 }
-template <int COLS>
-__device__ __forceinline__ void tmem_dealloc(unsigned taddr) {  // one full warp
-  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "n"(COLS) : "memory");
+__device__ __forceinline__ void tmem_dealloc(unsigned taddr, unsigned cols) {  // one full warp
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(cols) : "memory");
 }
 __device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
@@ -193,6 +191,50 @@ __device__ __forceinline__ void tmem_st4(unsigned taddr, const float (&r)[4]) {
 __device__ __forceinline__ void tmem_st8(unsigned taddr, const float (&r)[8]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(taddr), "f"(r[0]),
                "f"(r[1]), "f"(r[2]), "f"(r[3]), "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7]) : "memory");
+}
+
+// One thread-private record of W = 12 or 16 words at columns [taddr, taddr + W): load (asynchronous;
+// tm_rec_wait makes r valid -- it names r so no use of it can be scheduled before the wait) / store.
+template <int W>
+__device__ __forceinline__ void tm_rec_ld(unsigned taddr, float (&r)[W]) {
+  static_assert(W == 12 || W == 16, "records of 12 or 16 words");
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+               : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
+               : "r"(taddr));
+  if constexpr (W == 12)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+                 : "=f"(r[8]), "=f"(r[9]), "=f"(r[10]), "=f"(r[11]) : "r"(taddr + 8));
+  else
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+                 : "=f"(r[8]), "=f"(r[9]), "=f"(r[10]), "=f"(r[11]), "=f"(r[12]), "=f"(r[13]), "=f"(r[14]), "=f"(r[15])
+                 : "r"(taddr + 8));
+}
+template <int W>
+__device__ __forceinline__ void tm_rec_wait(float (&r)[W]) {
+  if constexpr (W == 12)
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+                 : "+f"(r[0]), "+f"(r[1]), "+f"(r[2]), "+f"(r[3]), "+f"(r[4]), "+f"(r[5]), "+f"(r[6]), "+f"(r[7]),
+                   "+f"(r[8]), "+f"(r[9]), "+f"(r[10]), "+f"(r[11])
+                 :
+                 : "memory");
+  else
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+                 : "+f"(r[0]), "+f"(r[1]), "+f"(r[2]), "+f"(r[3]), "+f"(r[4]), "+f"(r[5]), "+f"(r[6]), "+f"(r[7]),
+                   "+f"(r[8]), "+f"(r[9]), "+f"(r[10]), "+f"(r[11]), "+f"(r[12]), "+f"(r[13]), "+f"(r[14]), "+f"(r[15])
+                 :
+                 : "memory");
+}
+template <int W>
+__device__ __forceinline__ void tm_rec_st(unsigned taddr, const float (&r)[W]) {
+  static_assert(W == 12 || W == 16, "records of 12 or 16 words");
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(taddr), "f"(r[0]),
+               "f"(r[1]), "f"(r[2]), "f"(r[3]), "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7]) : "memory");
+  if constexpr (W == 12)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(taddr + 8), "f"(r[8]), "f"(r[9]),
+                 "f"(r[10]), "f"(r[11]) : "memory");
+  else
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(taddr + 8), "f"(r[8]),
+                 "f"(r[9]), "f"(r[10]), "f"(r[11]), "f"(r[12]), "f"(r[13]), "f"(r[14]), "f"(r[15]) : "memory");
 }
 
 template <int BYTES>

@@ -891,14 +891,17 @@ struct PointWork {
   }
   // TM: record k of this thread from tensor memory (warp-collective: every lane of the warp calls it)
   __device__ __forceinline__ void tm_load_pair(int k, C2 (&ya)[I], C2 (&yb)[I]) const {
-    static_assert(!TM || (I == 3 && sizeof(R) == 4), "tensor-memory records: complex64, I = 3");
-    float r8[8], r4[4];
-    tmem_ld8(tmy + k * TMW, r8);
-    tmem_ld4(tmy + k * TMW + 8, r4);
-    tmem_wait_ld(r8, r4);
-    ya[0] = mk<C2, R>(r8[0], r8[1]); yb[0] = mk<C2, R>(r8[2], r8[3]);
-    ya[1] = mk<C2, R>(r8[4], r8[5]); yb[1] = mk<C2, R>(r8[6], r8[7]);
-    ya[2] = mk<C2, R>(r4[0], r4[1]); yb[2] = mk<C2, R>(r4[2], r4[3]);
+    static_assert(!TM || ((I == 3 || I == 4) && sizeof(R) == 4), "tensor-memory records: complex64, I = 3 or 4");
+    if constexpr (TM) {
+      float r[TMW];
+      tm_rec_ld<TMW>(tmy + k * TMW, r);
+      tm_rec_wait<TMW>(r);
+#pragma unroll
+      for (int i = 0; i < I; ++i) {
+        ya[i] = mk<C2, R>(r[4 * i], r[4 * i + 1]);
+        yb[i] = mk<C2, R>(r[4 * i + 2], r[4 * i + 3]);
+      }
+    }
   }
   // q_b = |(P^H y)_b|^2 for both frames, as a pair
   __device__ __forceinline__ void q_pair(const C2 (&ya)[I], const C2 (&yb)[I], C2 (&q2)[I]) const {
@@ -1295,8 +1298,9 @@ __global__ void __launch_bounds__(256) slab_pack_kernel(const PackArgs a) {
 // one inner iteration) -- those paths compile out, which keeps the hot instantiations smaller
 // (instruction cache) and lighter on registers.  The launcher picks it when a call allows.
 template <typename R, int I, int JT, int G, bool RES, bool FAST = false, bool TM = false>
-__global__ void __launch_bounds__(TM ? 128 : 256, TM ? 4 : ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffca_loop_kernel(const LoopArgs a) {
-  static_assert(!TM || (FAST && RES && G == 4 && I == 3 && sizeof(R) == 4), "tensor-memory plan: the lean complex64 I = 3 loop");
+__global__ void __launch_bounds__(TM ? 128 : 256, (TM && I == 3) ? 4 : ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffca_loop_kernel(const LoopArgs a) {
+  static_assert(!TM || (FAST && RES && sizeof(R) == 4 && ((G == 4 && I == 3) || (G == 1 && I == 4))),
+                "tensor-memory plans: the lean complex64 loop, 4-bin CTAs at I = 3 or cluster CTAs at I = 4");
   using C2 = typename Cpx<R>::T;
   constexpr int JM = JT > 0 ? JT : 8;
   constexpr int IC = Shape<I, JM>::IC, NCH = Shape<I, JM>::NCH, NB = Shape<I, JM>::NB;
@@ -1366,15 +1370,17 @@ __global__ void __launch_bounds__(TM ? 128 : 256, TM ? 4 : ((I == 4 || (I > 4 &&
   // thread in flight at once.
   __shared__ unsigned long long gather_bar;
   // TM: the y records of the CTA's bins live in tensor memory as thread-private arrays (thread t
-  // owns frame pairs slot + k nslots, k < nrec, 4 I columns each): 128 columns x 128 lanes per CTA,
-  // four CTAs fill the SM's 512 columns.  Shared memory holds only the powers v.
+  // owns frame pairs slot + k nslots, k < nrec, 4 I columns each).  I = 3: 128 columns x 128 lanes
+  // per 4-bin CTA, four CTAs fill the SM's 512 columns.  I = 4 (cluster plans): 256 columns, two CTAs
+  // per SM, each holding twice the frames shared memory alone would.  Shared memory holds the powers v.
   __shared__ unsigned tm_base_s;
-  constexpr int TMCOLS = 128;
-  unsigned tmy = 0;
+  unsigned tmy = 0, tmcols = 0;
   const int nrec = (NLs / 2 + nslots - 1) / nslots;
   if constexpr (TM) {
-    if (nrec * 4 * I > TMCOLS || blockDim.x != 128) __trap();
-    if (tid < 32) tmem_alloc<TMCOLS>(&tm_base_s);
+    constexpr int TMW = 4 * I;
+    tmcols = nrec * TMW <= 128 ? 128u : (nrec * TMW <= 256 ? 256u : 512u);
+    if (nrec * TMW > 512 || blockDim.x != 128) __trap();
+    if (tid < 32) tmem_alloc(&tm_base_s, tmcols);
     tmem_fence_before();
     __syncthreads();
     tmem_fence_after();
@@ -1382,7 +1388,7 @@ __global__ void __launch_bounds__(TM ? 128 : 256, TM ? 4 : ((I == 4 || (I > 4 &&
 #pragma unroll 2
     for (int k = 0; k < nrec; ++k) {
       const int m = slot + k * nslots;
-      float r8[8], r4[4];
+      float r[TMW];
 #pragma unroll
       for (int i = 0; i < I; ++i)
 #pragma unroll
@@ -1390,12 +1396,10 @@ __global__ void __launch_bounds__(TM ? 128 : 256, TM ? 4 : ((I == 4 || (I > 4 &&
           const int n = 2 * m + par;
           C2 z = mk<C2, R>(R(0), R(0));
           if (active && n < NLr) z = __ldg(yg + ((u * I + i) * (long long)N + n0 + n) * F + f);
-          const int w = 4 * i + 2 * par;
-          if (w < 8) { r8[w] = z.x; r8[w + 1] = z.y; }
-          else { r4[w - 8] = z.x; r4[w - 7] = z.y; }
+          r[4 * i + 2 * par] = z.x;
+          r[4 * i + 2 * par + 1] = z.y;
         }
-      tmem_st8(tmy + k * 4 * I, r8);
-      tmem_st4(tmy + k * 4 * I + 8, r4);
+      tm_rec_st<TMW>(tmy + k * TMW, r);
     }
     tmem_wait_st();
   }
@@ -1503,15 +1507,13 @@ __global__ void __launch_bounds__(TM ? 128 : 256, TM ? 4 : ((I == 4 || (I > 4 &&
   if (a.vf_mode == 3) {
     R psum = R(0);
     if constexpr (TM) {  // own records (zero padding adds nothing); warp-collective loads
+      constexpr int TMW = 4 * I;
       for (int k = 0; k < nrec; ++k) {
-        float r8[8], r4[4];
-        tmem_ld8(tmy + k * 4 * I, r8);
-        tmem_ld4(tmy + k * 4 * I + 8, r4);
-        tmem_wait_ld(r8, r4);
+        float r[TMW];
+        tm_rec_ld<TMW>(tmy + k * TMW, r);
+        tm_rec_wait<TMW>(r);
 #pragma unroll
-        for (int w = 0; w < 8; ++w) psum = fma(R(r8[w]), R(r8[w]), psum);
-#pragma unroll
-        for (int w = 0; w < 4; ++w) psum = fma(R(r4[w]), R(r4[w]), psum);
+        for (int w = 0; w < TMW; ++w) psum = fma(R(r[w]), R(r[w]), psum);
       }
     } else if (active)
       for (int n = slot; n < NLr; n += nslots)
@@ -1955,7 +1957,7 @@ __global__ void __launch_bounds__(TM ? 128 : 256, TM ? 4 : ((I == 4 || (I > 4 &&
   if constexpr (TM) {
     tmem_fence_before();
     __syncthreads();
-    if (tid < 32) tmem_dealloc<TMCOLS>(tm_base_s);
+    if (tid < 32) tmem_dealloc(tm_base_s, tmcols);
   }
   // no CTA may exit while a peer can still read its shared memory
   if (C > 1) cg::this_cluster().sync();

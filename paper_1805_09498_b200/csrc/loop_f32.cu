@@ -12,6 +12,8 @@ template <int I, int J>
 static LoopFn hot(int G, bool res, bool fast, bool tm) {
   if constexpr (I == 3 && J == 3)
     if (tm) return (G == 4 && res && fast) ? (LoopFn)ffca_loop_kernel<float, 3, 3, 4, true, true, true> : nullptr;
+  if constexpr (I == 4 && J == 4)
+    if (tm) return (G == 1 && res && fast) ? (LoopFn)ffca_loop_kernel<float, 4, 4, 1, true, true, true> : nullptr;
   if constexpr (I <= 4) {
     if constexpr (I == 3 && J == 3)
       if (G == 4 && res && fast) return ffca_loop_kernel<float, I, J, 4, true, true>;
@@ -27,9 +29,9 @@ static LoopFn hot(int G, bool res, bool fast, bool tm) {
 }
 
 LoopFn loop_kernel_f32(int I, int J, int G, bool res, bool fast, bool tm) {
-  if (tm && !(I == 3 && J == 3)) return nullptr;
+  if (tm && !((I == 3 && J == 3) || (I == 4 && J == 4))) return nullptr;
   if (I == 3 && J == 3) return hot<3, 3>(G, res, fast, tm);
-  if (I == 4 && J == 4) return hot<4, 4>(G, res, fast, false);
+  if (I == 4 && J == 4) return hot<4, 4>(G, res, fast, tm);
   if (I == 8 && J == 6) return hot<8, 6>(G, res, fast, false);
   if (I == 2 && J == 2) return hot<2, 2>(G, res, false, false);
   if (J > 8 || G != 1) return nullptr;

@@ -7,7 +7,7 @@
 using namespace ffca;
 __global__ void k(float* o){
   __shared__ unsigned base;
-  if (threadIdx.x < 32) tmem_alloc<128>(&base);
+  if (threadIdx.x < 32) tmem_alloc(&base, 128);
   tmem_fence_before(); __syncthreads(); tmem_fence_after();
   unsigned t = base + (((threadIdx.x>>5)&3)*32u << 16);
   float r8[8], r4[4];
@@ -19,7 +19,7 @@ __global__ void k(float* o){
   float s=0; for(int i=0;i<8;++i) s+=a8[i]; for(int i=0;i<4;++i) s+=a4[i];
   o[threadIdx.x]=s;
   __syncthreads();
-  if (threadIdx.x < 32) tmem_dealloc<128>(base);
+  if (threadIdx.x < 32) tmem_dealloc(base, 128);
 }
 int main(){ float* d; cudaMalloc(&d, 128*4); k<<<1,128>>>(d); float h[128]; cudaMemcpy(h,d,512,cudaMemcpyDeviceToHost);
  int bad=0; for(int t=0;t<128;++t){ float e=12*t*100+66; if(h[t]!=e) bad++; } printf("err=%s bad=%d h[5]=%f\n", cudaGetErrorString(cudaGetLastError()), bad, h[5]); return bad; }

@@ -5,7 +5,7 @@ import torch
 from paper_1805_09498_b200 import _lib
 from paper_1805_09498_b200.workloads import CONFIGS, make_torch
 
-cfg = CONFIGS[3]
+cfg = CONFIGS[int(os.environ.get('CFG', '3'))]
 dev = torch.device("cuda", 0)
 lib = _lib.require_gpu()
 lib.ffca_set_kernel_timing(1)
@@ -13,7 +13,7 @@ code = _lib.C64
 
 
 def run(y, P0, l0, v0, mix, env, iters=cfg.iterations, N=cfg.N, F=cfg.F):
-    for k in ("FFCA_TMEM", "FFCA_FORCE_PLAN"):
+    for k in ("FFCA_NO_TMEM", "FFCA_FORCE_PLAN"):
         os.environ.pop(k, None)
     os.environ.update(env)
     P, l, v = torch.empty_like(P0), torch.empty_like(l0), torch.empty_like(v0)
@@ -33,9 +33,9 @@ def rel(a, b):
 
 mix = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 y, P0, l0, v0 = make_torch(cfg, 1, mix, dev)
-ref = run(y, P0, l0, v0, mix, {})
-tm = run(y, P0, l0, v0, mix, {"FFCA_TMEM": "1"})
-g4 = run(y, P0, l0, v0, mix, {"FFCA_FORCE_PLAN": "4,1,1,128"})
+ref = run(y, P0, l0, v0, mix, {"FFCA_NO_TMEM": "1"})
+tm = run(y, P0, l0, v0, mix, {})
+g4 = run(y, P0, l0, v0, mix, {"FFCA_FORCE_PLAN": "4,1,1,128"}) if cfg.I == 3 else ref
 print(json.dumps({"mix": mix, "ms_default": ref[3], "ms_tm": tm[3], "ms_g4_128": g4[3],
                   "tm_vs_default": [rel(tm[i], ref[i]) for i in range(3)],
                   "tm_vs_g4": [rel(tm[i], g4[i]) for i in range(3)],

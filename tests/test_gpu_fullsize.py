@@ -15,6 +15,8 @@ rel = max|a - b| / max|b| (test_fastfca.py:364-366); rel-L2 = ||a - b|| / ||b||.
 Reference loops: fastfca.py:401-474 (run_fastfca), fca.py:187-215 (run_fca).
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -45,21 +47,28 @@ def ll_hist(run):
     return np.array([run.loglik_init] + run.loglik_after_em + run.loglik_after_p)
 
 
-def check_fastfca(cfg, seed, F):
+_REF = {}
+
+
+def check_fastfca(cfg, seed, F, fp64=True):
     y, P0, lam0, v0, _ = mixture(seed, cfg.I, cfg.J, F, cfg.N, cfg.rank, cfg.zero_frac)
     T = cfg.iterations
-    ref = ffr.run_fastfca(y, P0, lam0, v0, iterations=T, record_likelihood=True)
+    key = (cfg.name, seed, F)
+    if key not in _REF:  # the oracle run is the slow part: once per case
+        ref = ffr.run_fastfca(y, P0, lam0, v0, iterations=T, record_likelihood=True)
+        _REF[key] = (ref, ffr.images(ref.P, ref.mu))
+    ref, ref_img = _REF[key]
     ref_ll = np.array([ref.loglik_init] + ref.loglik_after_em + ref.loglik_after_p)
-    ref_img = ffr.images(ref.P, ref.mu)
 
-    r64 = fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=T,
-                              record_likelihood=True)
-    ll = ll_hist(r64)
-    assert len(ll) == 1 + 2 * T
-    assert np.abs(ll - ref_ll).max() <= 1e-6 * np.abs(ref_ll).max()
-    assert abs(ll[-1] - ref_ll[-1]) <= 1e-6 * abs(ref_ll[-1])
-    for got, want in ((r64.params.P, ref.P), (r64.params.Lam, ref.lam), (r64.params.v, ref.v)):
-        assert rel(got, want) <= 1e-9
+    if fp64:
+        r64 = fastfca.run_fastfca(ObservationTensor(y), fastfca.FastFcaParams(P0, lam0, v0), iterations=T,
+                                  record_likelihood=True)
+        ll = ll_hist(r64)
+        assert len(ll) == 1 + 2 * T
+        assert np.abs(ll - ref_ll).max() <= 1e-6 * np.abs(ref_ll).max()
+        assert abs(ll[-1] - ref_ll[-1]) <= 1e-6 * abs(ref_ll[-1])
+        for got, want in ((r64.params.P, ref.P), (r64.params.Lam, ref.lam), (r64.params.v, ref.v)):
+            assert rel(got, want) <= 1e-9
 
     y32, P32, l32, v32 = c64(y, P0, lam0, v0)
     r32 = fastfca.run_fastfca(ObservationTensor(y32), fastfca.FastFcaParams(P32, l32, v32), iterations=T)
@@ -72,13 +81,30 @@ def check_fastfca(cfg, seed, F):
     return r32
 
 
+def plan8(I, J, N, F, lean):
+    out = np.zeros(8, np.int32)
+    _lib.load().ffca_plan_loop_ex(0, _lib.C64, 1, I, J, N, F, _lib.VF_AUTO, lean, out.ctypes.data_as(_lib._ip))
+    return {"G": int(out[0]), "C": int(out[1]), "threads": int(out[3]), "tm": int(out[6]), "tmcols": int(out[7])}
+
+
 def test_config2_long_recording_full_30_iterations():
     # config 2: I = J = 4, N = 9375, rank-8 NMF, complex64, 30 iterations, on 12 bins; one bin
-    # exceeds a CTA's shared memory, so the default plan splits its frames over an 8-CTA cluster
-    # (DSMEM reductions in rank order twice per iteration)
+    # exceeds a CTA's shared memory.  The plain loop keeps the y records in tensor memory (256
+    # columns per CTA) and splits a bin over a 4-CTA cluster; shared memory alone (the loop with the
+    # likelihood record, or FFCA_NO_TMEM) needs an 8-CTA cluster.  DSMEM reductions in rank order
+    # twice per iteration either way; both plans are held to the same tolerances.
     cfg = CONFIGS[2]
-    assert plan(_lib.C64, cfg.I, cfg.J, cfg.N, 12)["C"] == 8
-    check_fastfca(cfg, 2, 12)
+    p = plan8(cfg.I, cfg.J, cfg.N, 12, 1)
+    assert p["C"] == 4 and p["tm"] == 1 and p["tmcols"] == 256 and p["threads"] == 128
+    assert plan8(cfg.I, cfg.J, cfg.N, 12, 0)["C"] == 8 and plan8(cfg.I, cfg.J, cfg.N, 12, 0)["tm"] == 0
+    r_tm = check_fastfca(cfg, 2, 12)
+    os.environ["FFCA_NO_TMEM"] = "1"
+    try:
+        assert plan(_lib.C64, cfg.I, cfg.J, cfg.N, 12)["C"] == 8
+        r_sm = check_fastfca(cfg, 2, 12, fp64=False)
+    finally:
+        os.environ.pop("FFCA_NO_TMEM", None)
+    assert rel(r_tm.params.P, r_sm.params.P) <= 1e-5 and rel(r_tm.params.v, r_sm.params.v) <= 1e-5
 
 
 def test_config4_large_array_full_20_iterations():

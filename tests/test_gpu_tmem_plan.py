@@ -109,3 +109,37 @@ def test_plans_that_do_not_use_tensor_memory():
     long_args = batch(1, 6, 642, 23)
     P = fastfca.run_fastfca_batch(*long_args, iterations=3)[0]
     assert np.isfinite(P).all()
+
+
+# ---------------------------------------------------------------------------
+# I = J = 4: cluster plans with the y records in tensor memory (config 2's plan)
+# ---------------------------------------------------------------------------
+
+
+def plan8_44(F, N, lean=1):
+    out = np.zeros(8, np.int32)
+    assert _lib.load().ffca_plan_loop_ex(0, _lib.C64, 1, 4, 4, N, F, _lib.VF_AUTO, lean,
+                                         out.ctypes.data_as(_lib._ip)) == 0
+    return [int(x) for x in out]
+
+
+@pytest.mark.parametrize("N,C", [(2200, 2), (2201, 2), (4101, 2), (8200, 4)])
+def test_cluster_tmem_plan_i4(N, C):
+    # bins too long for one CTA's shared memory: a C-CTA cluster, 256 tensor-memory columns per CTA;
+    # uneven frame splits and odd frame counts (half-filled last pair on one rank)
+    F = 3
+    p = plan8_44(F, N)
+    assert p[0] == 1 and p[1] == C and p[3] == 128 and p[6] == 1 and p[7] == 256
+    y, P0, lam0, v0, _ = mixture(500 + N, 4, 4, F, N, 8, 0.0)
+    a32 = (y.astype(np.complex64)[None], P0.astype(np.complex64)[None], lam0.astype(np.float32)[None],
+           v0.astype(np.float32)[None])
+    tm = fastfca.run_fastfca_batch(*a32, iterations=4)[:3]
+    again = fastfca.run_fastfca_batch(*a32, iterations=4)[:3]
+    os.environ["FFCA_NO_TMEM"] = "1"
+    assert plan8_44(F, N)[6] == 0
+    sm = fastfca.run_fastfca_batch(*a32, iterations=4)[:3]
+    ref = ffr.run_fastfca(y, P0, lam0, v0, iterations=4, stats=False)
+    for a, b, c, want in zip(tm, sm, again, (ref.P, ref.lam, ref.v)):
+        assert np.array_equal(a, c)
+        assert rel(a, b) <= 1e-5
+        assert rel(a[0], want) <= 1e-4
