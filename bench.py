@@ -424,7 +424,7 @@ def run_ours(args, D):
         "effective_streaming_GBps": round(streaming / (k_ms / 1e3) / 1e9, 1),
         "effective_streaming_note": ("SURVEY §8(d) two-pass streaming model, 2*I*c + 3*J*r = "
                                      f"{2 * I * c + 3 * J * r} B per TF-point-iteration; a model figure, not DRAM "
-                                     "traffic -- the kernel holds each bin in shared memory for the whole run"),
+                                     "traffic -- the kernel holds each bin on chip (y in tensor memory, v in shared memory) for the whole run"),
         "binding": None,
     }
     # compute roofline of the same launch: algorithmic FP32 flops of the formulation per TF-point
@@ -444,7 +444,8 @@ def run_ours(args, D):
     if prof:
         clk = (clocks or {}).get("sm_mhz") or 1965.0
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        binding = {"resource": "FP32 issue (point phases) + per-bin reductions / fp64 solves",
+        binding = {"resource": "FP32 FMA pipe / issue in the point phases at the 16 warps per SM the registers allow, "
+                               "+ per-bin reductions / fp64 solves",
                    "source": prof.get("source")}
         if prof.get("warp_instructions_per_launch"):
             binding["issue_frac"] = round(prof["warp_instructions_per_launch"] / (4 * sms * clk * 1e6 * k_ms / 1e3), 3)

@@ -114,7 +114,13 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
   // complex64, I = J = 3, lean loop, N <= 640: 4-bin CTAs of 128 threads (32 per bin, 10 frame pairs
   // per thread) with the y records in tensor memory -- 16 bins per SM instead of the 8 that shared
   // memory alone holds, at the same 16 warps.
-  if (dtype == FFCA_C64 && I == 3 && J == 3 && G0 == 4 && fast && vf_mode != 2 && N <= 640 && !getenv("FFCA_NO_TMEM")) {
+  // Worth it from one full wave of 16 bins per SM on (measured on B200, config-3 shape: 1 / 2 / 4 / 8
+  // mixtures 0.129 / 0.165 / 0.253 / 0.431 ms against 0.098 / 0.154 / 0.249 / 0.473 ms for the 2-bin
+  // shared-memory plan); FFCA_TMEM_MIN_BINS overrides the threshold (tests use 0).
+  long long tm_min_bins = 16LL * nsm;
+  if (const char* e = getenv("FFCA_TMEM_MIN_BINS")) tm_min_bins = atoll(e);
+  if (dtype == FFCA_C64 && I == 3 && J == 3 && G0 == 4 && fast && vf_mode != 2 && N <= 640 && total_bins >= tm_min_bins &&
+      !getenv("FFCA_NO_TMEM")) {
     fill(4, 1, true);
     p.threads = 128;
     p.tm = true;

@@ -59,6 +59,9 @@ def test_plan_introspection_without_device():
     assert out[0] == 4 and out[1] == 1 and out[3] == 128 and out[4] == 1 and out[5] < 48 * 1024
     assert lib.ffca_plan_loop_ex(0, _lib.C64, 256, 3, 3, 626, 513, _lib.VF_AUTO, 1, out8.ctypes.data_as(_lib._ip)) == 0
     assert list(out8[:6]) == list(out) and out8[6] == 1 and out8[7] == 128
+    # ... from one wave of 16 bins per SM on; a single mixture keeps 2 bins per CTA in shared memory
+    assert lib.ffca_plan_loop_ex(0, _lib.C64, 1, 3, 3, 626, 513, _lib.VF_AUTO, 1, out8.ctypes.data_as(_lib._ip)) == 0
+    assert out8[0] == 2 and out8[3] == 128 and out8[6] == 0
     # ... the loop with the likelihood record keeps 2 bins per 128-thread CTA in shared memory
     assert lib.ffca_plan_loop_ex(0, _lib.C64, 256, 3, 3, 626, 513, _lib.VF_AUTO, 0, out8.ctypes.data_as(_lib._ip)) == 0
     assert out8[0] == 2 and out8[3] == 128 and out8[4] == 1 and out8[6] == 0

@@ -18,12 +18,13 @@ from paper_1805_09498_b200.workloads import mixture
 
 pytestmark = pytest.mark.gpu
 
-ENV = ("FFCA_FORCE_PLAN", "FFCA_NO_TMEM")
+ENV = ("FFCA_FORCE_PLAN", "FFCA_NO_TMEM", "FFCA_TMEM_MIN_BINS")
 
 
 @pytest.fixture(autouse=True)
 def _plan_env():
     old = {k: os.environ.pop(k, None) for k in ENV}
+    os.environ["FFCA_TMEM_MIN_BINS"] = "0"  # the plan is chosen from one wave of bins on; small cases force it
     yield
     for k in ENV:
         os.environ.pop(k, None)
@@ -91,6 +92,15 @@ def test_tmem_plan_zero_cells_stay_finite():
     ref = ffr.run_fastfca(y[1].astype(np.complex128), P0[1].astype(np.complex128), lam0[1].astype(np.float64),
                           v0[1].astype(np.float64), iterations=10, stats=False)
     assert rel(P[1], ref.P) <= 1e-4 and rel(v[1], ref.v) <= 1e-4
+
+
+def test_small_batches_keep_the_shared_memory_plan():
+    # below one wave of 16 bins per SM the 2-bin shared-memory plan is faster (abi_fastfca.cu plan_loop)
+    os.environ.pop("FFCA_TMEM_MIN_BINS")
+    assert plan8(1, 513, 626)[6] == 0 and plan8(1, 513, 626)[0] == 2
+    assert plan8(256, 513, 626)[6] == 1
+    os.environ["FFCA_TMEM_MIN_BINS"] = "0"
+    assert plan8(1, 513, 626)[6] == 1
 
 
 def test_plans_that_do_not_use_tensor_memory():
