@@ -370,37 +370,51 @@ __global__ void __launch_bounds__(TILE_F* TILE_WARPS, 2) point_tile_kernel(const
         }
         if constexpr (MODE == PM_STATS) {
           const long long base = ((u * J + j) * rowN + (long long)n * F + f0) * I;  // first element of the run
-#pragma unroll
+          // The run starts on a 16-byte boundary for one frame in two (mu, complex64) / four (phi,
+          // fp32) only (odd F, I = 3), and ncu showed the element-wise fallback of the other runs
+          // as a third of the kernel's instructions.  So a run is staged SHIFTED: its h elements before
+          // the first 16-byte boundary (h < 16 / element size; they belong to the first lanes) are
+          // stored straight from registers, element e >= h goes to stage[e - h], and the aligned body
+          // leaves as 16-byte vectors (fixed trip count, predicated) with a ragged tail of < 16 bytes.
           C2* stage_mu = &ry[wp][sl][0][0];
           R* stage_phi = &rv[wp][sl][0][0];
+          const int ne = nlive * I;  // complex (real) elements of this run
+          C2* omu = a.out0 ? (C2*)a.out0 + base : nullptr;
+          R* oph = a.out1 ? (R*)a.out1 + base : nullptr;
+          constexpr int PM = 16 / int(sizeof(C2)), PP = 16 / int(sizeof(R));  // elements per 16-byte vector
+          const int hm = int(((16 - (reinterpret_cast<uintptr_t>(omu) & 15)) & 15) / sizeof(C2));
+          const int hp = int(((16 - (reinterpret_cast<uintptr_t>(oph) & 15)) & 15) / sizeof(R));
           __syncwarp();  // every lane has read this slot's y / v (and the previous source's run)
+#pragma unroll
           for (int i = 0; i < I; ++i) {
-            stage_mu[lane * I + i] = mu[i];
-            stage_phi[lane * I + i] = ph[i];
+            const int e = lane * I + i;
+            if (e >= hm) stage_mu[e - hm] = mu[i];
+            else if (omu && e < ne) omu[e] = mu[i];
+            if (e >= hp) stage_phi[e - hp] = ph[i];
+            else if (oph && e < ne) oph[e] = ph[i];
           }
           __syncwarp();
-          const int ne = nlive * I;  // complex (real) elements of this run
-          if (a.out0) {
-            C2* o = (C2*)a.out0 + base;
-            constexpr int PER = 16 / sizeof(C2);  // complex per 16-byte vector (2 for c64, 1 for c128)
-            const bool vec = ((reinterpret_cast<uintptr_t>(o) & 15) == 0) && (ne % PER == 0);
-            if (vec) {
-              for (int e = lane; e < ne / PER; e += 32)
-                reinterpret_cast<float4*>(o)[e] = reinterpret_cast<const float4*>(stage_mu)[e];
-            } else {
-              for (int e = lane; e < ne; e += 32) o[e] = stage_mu[e];
+          if (omu) {
+            const int nb = ne > hm ? ne - hm : 0, nv = nb / PM, r = nb - nv * PM;
+            float4* o = reinterpret_cast<float4*>(omu + hm);
+            constexpr int IT = (I * TILE_F / PM + 31) / 32;  // fixed trip count: compact predicated code
+#pragma unroll
+            for (int t = 0; t < IT; ++t) {
+              const int e = lane + 32 * t;
+              if (e < nv) o[e] = reinterpret_cast<const float4*>(stage_mu)[e];
             }
+            if (lane < r) omu[hm + nv * PM + lane] = stage_mu[nv * PM + lane];
           }
-          if (a.out1) {
-            R* o = (R*)a.out1 + base;
-            constexpr int PER = 16 / sizeof(R);
-            const bool vec = ((reinterpret_cast<uintptr_t>(o) & 15) == 0) && (ne % PER == 0);
-            if (vec) {
-              for (int e = lane; e < ne / PER; e += 32)
-                reinterpret_cast<float4*>(o)[e] = reinterpret_cast<const float4*>(stage_phi)[e];
-            } else {
-              for (int e = lane; e < ne; e += 32) o[e] = stage_phi[e];
+          if (oph) {
+            const int nb = ne > hp ? ne - hp : 0, nv = nb / PP, r = nb - nv * PP;
+            float4* o = reinterpret_cast<float4*>(oph + hp);
+            constexpr int IT = (I * TILE_F / PP + 31) / 32;
+#pragma unroll
+            for (int t = 0; t < IT; ++t) {
+              const int e = lane + 32 * t;
+              if (e < nv) o[e] = reinterpret_cast<const float4*>(stage_phi)[e];
             }
+            if (lane < r) oph[hp + nv * PP + lane] = stage_phi[nv * PP + lane];
           }
           __syncwarp();
         } else {
