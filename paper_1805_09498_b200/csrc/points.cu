@@ -439,6 +439,184 @@ __global__ void __launch_bounds__(TILE_F* TILE_WARPS, 2) point_tile_kernel(const
   }
 }
 
+// Statistics refresh / Wiener images for 4 < I <= 8, bin-tiled.  The per-bin constants no longer fit
+// registers (P and Q = P^-H are I x I complex each), so the CTA keeps them for its 32 bins in shared
+// memory, element-major with the bin fastest ([x * I + b][lane]: every lane reads its own bin's
+// element, conflict free), converted to the compute type once.  A CTA owns 32 consecutive bins x a
+// block of frames (blockIdx.y), its 8 warps stride the frames two at a time so that every P / Q /
+// lambda element read from shared memory feeds two points.  Statistics leave as each lane's I
+// consecutive elements of the (..., F, I) layout (16-byte vectors when I is even), images as
+// coalesced 32-bin rows of each (source, channel) plane.
+// (The untiled point_kernel re-read the fp64 Q of its bin from global memory for every point and
+// back-solved in fp64: config-4 shape images 13.8 ms, statistics 4.8 ms.)
+template <typename R, int I, int MODE>
+__global__ void __launch_bounds__(256) point_tile_big_kernel(const PointArgs a, int frames_per_cta) {
+  using C2 = typename Cpx<R>::T;
+  constexpr int JMAX = 8;
+  extern __shared__ __align__(16) unsigned char big_sm[];
+  C2* Ps = (C2*)big_sm;
+  C2* Qs = Ps + I * I * 32;
+  R* Ls = (R*)(Qs + (MODE == PM_IMAGES ? I * I * 32 : 0));
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int F = a.F, N = a.N, J = a.J;
+  const int ftiles = (F + 31) / 32;
+  const long long u = blockIdx.x / ftiles;
+  const int f0 = int(blockIdx.x % ftiles) * 32;
+  const int n_lo = blockIdx.y * frames_per_cta;
+  const int n_hi = n_lo + frames_per_cta < N ? n_lo + frames_per_cta : N;
+  const bool live = f0 + lane < F;
+  const int f = live ? f0 + lane : F - 1;
+  // per-bin constants of the tile -> shared memory (global reads coalesced over a bin's elements)
+  for (int e = threadIdx.x; e < 32 * I * I; e += blockDim.x) {
+    const int lb = e / (I * I), el = e % (I * I);
+    const int fb = f0 + lb < F ? f0 + lb : F - 1;
+    Ps[el * 32 + lb] = ((const C2*)a.P)[(u * F + fb) * I * I + el];
+    if constexpr (MODE == PM_IMAGES) {
+      const double2 q = ((const double2*)a.Q)[(u * F + fb) * I * I + el];
+      Qs[el * 32 + lb] = mk<C2, R>(R(q.x), R(q.y));
+    }
+  }
+  for (int e = threadIdx.x; e < 32 * J * I; e += blockDim.x) {
+    const int lb = e / (J * I), el = e % (J * I);  // el = j * I + i
+    const int fb = f0 + lb < F ? f0 + lb : F - 1;
+    Ls[el * 32 + lb] = ((const R*)a.lam)[((u * J + el / I) * F + fb) * I + el % I];
+  }
+  __syncthreads();
+  const R wfl = Floors<R>::weight;
+  const long long rowN = (long long)N * F;
+  const C2* __restrict__ yb = (const C2*)a.y + u * I * rowN;
+  const R* __restrict__ vb = (const R*)a.v + u * J * rowN;
+  // frames per step and warp: two where the registers allow (complex64 statistics), else one
+  constexpr int FP = (sizeof(R) == 4 && MODE == PM_STATS) ? 2 : 1;
+#pragma unroll 1
+  for (int n = n_lo + FP * wp; n < n_hi; n += 8 * FP) {
+    long long o[FP];
+    bool ok[FP];
+#pragma unroll
+    for (int r = 0; r < FP; ++r) {
+      ok[r] = n + r < n_hi;  // a missing second frame is computed on the first one again, not stored
+      o[r] = (long long)(ok[r] ? n + r : n) * F + f;
+    }
+    C2 y[FP][I], t[FP][I];  // y, y_t = P^H y
+#pragma unroll
+    for (int r = 0; r < FP; ++r)
+#pragma unroll
+      for (int i = 0; i < I; ++i) {
+        y[r][i] = yb[i * rowN + o[r]];
+        t[r][i] = mk<C2, R>(R(0), R(0));
+      }
+#pragma unroll
+    for (int x = 0; x < I; ++x)
+#pragma unroll
+      for (int b = 0; b < I; ++b) {
+        const C2 pe = Ps[(x * I + b) * 32 + lane];
+#pragma unroll
+        for (int r = 0; r < FP; ++r) cmac_conj(t[r][b], pe, y[r][x]);
+      }
+    R w[FP][I];
+#pragma unroll
+    for (int r = 0; r < FP; ++r)
+#pragma unroll
+      for (int i = 0; i < I; ++i) w[r][i] = R(0);
+    for (int j = 0; j < J; ++j) {
+      R v[FP];
+#pragma unroll
+      for (int r = 0; r < FP; ++r) v[r] = vb[j * rowN + o[r]];
+#pragma unroll
+      for (int i = 0; i < I; ++i) {
+        const R l = Ls[(j * I + i) * 32 + lane];
+#pragma unroll
+        for (int r = 0; r < FP; ++r) w[r][i] = fma(v[r], l, w[r][i]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < FP; ++r)
+#pragma unroll
+      for (int i = 0; i < I; ++i) w[r][i] = fmax(w[r][i], wfl);
+    for (int j = 0; j < J; ++j) {
+      R v[FP];
+#pragma unroll
+      for (int r = 0; r < FP; ++r) v[r] = vb[j * rowN + o[r]];
+      C2 m[FP][I];
+      R ph[FP][I];
+#pragma unroll
+      for (int i = 0; i < I; ++i) {
+        const R l = Ls[(j * I + i) * 32 + lane];
+#pragma unroll
+        for (int r = 0; r < FP; ++r) {
+          // phi = a (1 - a / w) as a (w - a) / w: exact 0 for a single source (w = a), where
+          // 1 - a * (1 / w) would leave the reciprocal's rounding error (the reference divides)
+          const R aa = v[r] * l;
+          const R iw = rcp(w[r][i]);
+          const R g = aa * iw;
+          m[r][i] = mk<C2, R>(g * t[r][i].x, g * t[r][i].y);
+          ph[r][i] = fmax(aa * (w[r][i] - aa) * iw, R(0));
+        }
+      }
+      if constexpr (MODE == PM_STATS) {
+#pragma unroll
+        for (int r = 0; r < FP; ++r) {
+          if (!(live && ok[r])) continue;
+          const long long base = ((u * J + j) * rowN + o[r]) * I;
+          if (a.out0) {
+            C2* d = (C2*)a.out0 + base;
+            if constexpr (sizeof(C2) == 8 && I % 2 == 0) {  // I complex64 = I / 2 aligned 16-byte vectors
+#pragma unroll
+              for (int i = 0; i < I; i += 2)
+                reinterpret_cast<float4*>(d)[i / 2] = make_float4(float(m[r][i].x), float(m[r][i].y), float(m[r][i + 1].x), float(m[r][i + 1].y));
+            } else {
+#pragma unroll
+              for (int i = 0; i < I; ++i) d[i] = m[r][i];
+            }
+          }
+          if (a.out1) {
+            R* d = (R*)a.out1 + base;
+            if constexpr (sizeof(R) == 4 && I % 4 == 0) {
+#pragma unroll
+              for (int i = 0; i < I; i += 4)
+                reinterpret_cast<float4*>(d)[i / 4] = make_float4(float(ph[r][i]), float(ph[r][i + 1]), float(ph[r][i + 2]), float(ph[r][i + 3]));
+            } else {
+#pragma unroll
+              for (int i = 0; i < I; ++i) d[i] = ph[r][i];
+            }
+          }
+        }
+      } else {
+        C2* __restrict__ out = (C2*)a.out0 + (u * J + j) * I * rowN;
+#pragma unroll 1  // (fully unrolled, the compiler hoists all I * I Q loads and spills)
+        for (int x = 0; x < I; ++x) {
+          C2 acc[FP];
+#pragma unroll
+          for (int r = 0; r < FP; ++r) acc[r] = mk<C2, R>(R(0), R(0));
+#pragma unroll
+          for (int b = 0; b < I; ++b) {  // acc += Q[x][b] mu[b]
+            const C2 q = Qs[(x * I + b) * 32 + lane];
+#pragma unroll
+            for (int r = 0; r < FP; ++r) {
+              acc[r].x = fma(q.x, m[r][b].x, fma(-q.y, m[r][b].y, acc[r].x));
+              acc[r].y = fma(q.x, m[r][b].y, fma(q.y, m[r][b].x, acc[r].y));
+            }
+          }
+#pragma unroll
+          for (int r = 0; r < FP; ++r)
+            if (live && ok[r]) out[x * rowN + o[r]] = acc[r];
+        }
+      }
+    }
+  }
+}
+
+template <typename R, int MODE>
+static void* big_tile_fn(int I) {
+  switch (I) {
+    case 5: return (void*)point_tile_big_kernel<R, 5, MODE>;
+    case 6: return (void*)point_tile_big_kernel<R, 6, MODE>;
+    case 7: return (void*)point_tile_big_kernel<R, 7, MODE>;
+    case 8: return (void*)point_tile_big_kernel<R, 8, MODE>;
+  }
+  return nullptr;
+}
+
 template <typename R, int MODE>
 static void* tile_fn(int I) {
   switch (I) {
@@ -524,6 +702,28 @@ int launch_points(int dtype, const PointArgs& a, cudaStream_t s) {
     const long long blocks = (long long)a.U * ((a.F + TS - 1) / TS);
     void* args[] = {(void*)&a};
     FFCA_CK(cudaLaunchKernel(tf, dim3(unsigned(blocks)), dim3(TILE_F * TILE_WARPS), args, 0, s));
+    count_launch();
+    return FFCA_OK;
+  }
+  if ((a.mode == PM_STATS || a.mode == PM_IMAGES) && a.I > 4 && a.I <= 8 && a.J <= 8) {
+    void* tf = nullptr;
+    if (a.mode == PM_STATS)
+      tf = dtype == FFCA_C64 ? big_tile_fn<float, PM_STATS>(a.I) : big_tile_fn<double, PM_STATS>(a.I);
+    else
+      tf = dtype == FFCA_C64 ? big_tile_fn<float, PM_IMAGES>(a.I) : big_tile_fn<double, PM_IMAGES>(a.I);
+    const size_t cs = dtype == FFCA_C64 ? 8 : 16, rs = cs / 2;
+    const size_t smem = size_t(32) * a.I * a.I * cs * (a.mode == PM_IMAGES ? 2 : 1) + size_t(32) * a.J * a.I * rs;
+    const long long tiles = (long long)a.U * ((a.F + 31) / 32);
+    // frame blocks: enough CTAs to fill the device (~8 per SM), at least 32 frames each, even count
+    int nsplit = int((8LL * 148 + tiles - 1) / tiles);
+    if (nsplit > (a.N + 31) / 32) nsplit = (a.N + 31) / 32;
+    if (nsplit < 1) nsplit = 1;
+    int fpc = (a.N + nsplit - 1) / nsplit;
+    fpc = (fpc + 15) / 16 * 16;  // whole steps of the 8 warps x 1 or 2 frames
+    nsplit = (a.N + fpc - 1) / fpc;
+    if (smem > 48 * 1024) FFCA_CK(cudaFuncSetAttribute(tf, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    void* args[] = {(void*)&a, (void*)&fpc};
+    FFCA_CK(cudaLaunchKernel(tf, dim3(unsigned(tiles), unsigned(nsplit)), dim3(256), args, smem, s));
     count_launch();
     return FFCA_OK;
   }

@@ -8,8 +8,9 @@ from paper_1805_09498_b200 import _lib
 from paper_1805_09498_b200.workloads import CONFIGS, make_torch
 
 code_name = sys.argv[1] if len(sys.argv) > 1 else "c64"
-cfg = CONFIGS[3]
-U, I, J, N, F = 256 if code_name == "c64" else 64, cfg.I, cfg.J, cfg.N, cfg.F
+cfg = CONFIGS[int(os.environ.get("CFG", "3"))]  # CFG=4: the I = 8, J = 6 shape (untiled point_kernel path)
+U = (256 if code_name == "c64" else 64) if cfg.mixtures > 1 else 1
+U, I, J, N, F = int(os.environ.get("MIX", U)), cfg.I, cfg.J, cfg.N, cfg.F
 dev = torch.device("cuda", 0)
 lib = _lib.require_gpu()
 y, P, lam, v = make_torch(cfg, 5, U, dev)
@@ -49,6 +50,6 @@ pts = U * N * F
 b_img = pts * (I * cs + J * rs + J * I * cs)
 b_st = pts * (I * cs + J * rs + J * I * (cs + rs))
 ti, ts = timeit(images), timeit(stats)
-print(json.dumps({"what": f"{U} mixtures x (I=J=3, F=513, N=626) {code_name}, device-resident",
+print(json.dumps({"what": f"{U} mixtures x (I={I}, J={J}, F={F}, N={N}) {code_name}, device-resident",
                   "images_ms": round(ti, 3), "images_GBps": round(b_img / ti / 1e6, 1),
                   "stats_ms": round(ts, 3), "stats_GBps": round(b_st / ts / 1e6, 1), "hbm_peak_GBps": 6549.1}))
