@@ -161,7 +161,7 @@ constexpr int tile_depth() {
 }
 
 template <typename R, int I, int MODE>
-__global__ void __launch_bounds__(TILE_F* TILE_WARPS, 2) point_tile_kernel(const PointArgs a) {
+__global__ void __launch_bounds__(TILE_F* TILE_WARPS, 2) point_tile_kernel(const PointArgs a, int frames_per_cta) {
   using C2 = typename Cpx<R>::T;
   constexpr int JMAX = 4;
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
@@ -211,7 +211,11 @@ __global__ void __launch_bounds__(TILE_F* TILE_WARPS, 2) point_tile_kernel(const
   // instruction covers whole sectors.  The slot is refilled only by the next iteration's issue.
   __shared__ __align__(16) C2 ry[TILE_WARPS][TILE_D][I][TILE_F];
   __shared__ __align__(16) R rv[TILE_WARPS][TILE_D][JMAX][TILE_F];
-  const int nfr = N > wp ? (N - wp + TILE_WARPS - 1) / TILE_WARPS : 0;  // frames of this warp
+  // frames [n_lo, n_hi) of this CTA (blockIdx.y; frames_per_cta is a multiple of TILE_WARPS): a single
+  // long mixture would otherwise run on F / 32 CTAs only (config-2 shape: 33 CTAs on 148 SMs)
+  const int n_lo = blockIdx.y * frames_per_cta;
+  const int n_cnt = (n_lo + frames_per_cta < N ? frames_per_cta : N - n_lo);
+  const int nfr = n_cnt > wp ? (n_cnt - wp + TILE_WARPS - 1) / TILE_WARPS : 0;  // frames of this warp
   if constexpr (MODE == PM_IMAGES && sizeof(R) == 4) {
     // complex64 images.  Measured: the generic loop below spends 59 % of its 467 SASS instructions per
     // frame on integer work -- 64-bit indices re-derived for every load and store, and the sector
@@ -230,7 +234,7 @@ __global__ void __launch_bounds__(TILE_F* TILE_WARPS, 2) point_tile_kernel(const
     C2* outu = (C2*)a.out0 + u * J * I * rowN;  // this mixture's images
     asm volatile("" : "+l"(ybo), "+l"(vbo), "+l"(outu));
     const int ostep = TILE_WARPS * F;  // elements between a warp's consecutive frames
-    int oi = wp * F + f, ki = 0;       // next frame to request: element offset in a plane, index
+    int oi = (n_lo + wp) * F + f, ki = 0;  // next frame to request: element offset in a plane, index
     auto issue = [&]() {
       const bool ok = ki < nfr;
       const int o = ok ? oi : 0;
@@ -247,13 +251,13 @@ __global__ void __launch_bounds__(TILE_F* TILE_WARPS, 2) point_tile_kernel(const
     unsigned ownmask = 0;
 #pragma unroll
     for (int p = 0; p < JMAX * I; ++p) {
-      const long long e = (u * J * I + p) * rowN + (long long)wp * F + f;  // this thread's first element of plane p
+      const long long e = (u * J * I + p) * rowN + (long long)(n_lo + wp) * F + f;  // this thread's first element of plane p
       // first bin of this element's 32-byte sector; the tile owning that bin writes the sector
       const int b0 = f - int(e & (EPS - 1));
       const bool own = live && (TS == TILE_F || ((b0 >= f0 || f0 == 0) && (b0 < f0 + TS || last_tile)));
       ownmask |= unsigned(own) << p;
     }
-    int oc = wp * F + f;  // element offset (in a plane) of the frame being consumed
+    int oc = (n_lo + wp) * F + f;  // element offset (in a plane) of the frame being consumed
 #pragma unroll
     for (int k = 0; k < TILE_D - 1; ++k) issue();
 #pragma unroll 1
@@ -310,7 +314,7 @@ __global__ void __launch_bounds__(TILE_F* TILE_WARPS, 2) point_tile_kernel(const
     }
   } else {
     auto issue = [&](int k) {
-      const int n = wp + k * TILE_WARPS;
+      const int n = n_lo + wp + k * TILE_WARPS;
       const bool ok = k < nfr;
       const long long o = ok ? (long long)n * F + f : 0;
       const int sl = k % TILE_D;
@@ -327,7 +331,7 @@ __global__ void __launch_bounds__(TILE_F* TILE_WARPS, 2) point_tile_kernel(const
     for (int k = 0; k < nfr; ++k) {
       issue(k + TILE_D - 1);
       cp_async_wait<TILE_D - 1>();
-      const int n = wp + k * TILE_WARPS;
+      const int n = n_lo + wp + k * TILE_WARPS;
       const int sl = k % TILE_D;
       const long long off = (long long)n * F + f;
       C2 yv[I];
@@ -700,8 +704,15 @@ int launch_points(int dtype, const PointArgs& a, cudaStream_t s) {
     const int TS = a.mode == PM_IMAGES ? (dtype == FFCA_C64 ? tile_stride<float, PM_IMAGES>() : tile_stride<double, PM_IMAGES>())
                                        : TILE_F;
     const long long blocks = (long long)a.U * ((a.F + TS - 1) / TS);
-    void* args[] = {(void*)&a};
-    FFCA_CK(cudaLaunchKernel(tf, dim3(unsigned(blocks)), dim3(TILE_F * TILE_WARPS), args, 0, s));
+    // frame blocks (grid.y): about 8 CTAs per SM in total, at least 64 frames each, whole steps of the warps
+    int nsplit = int((8LL * 148 + blocks - 1) / blocks);
+    if (nsplit > a.N / 64) nsplit = a.N / 64;
+    if (nsplit < 1) nsplit = 1;
+    int fpc = (a.N + nsplit - 1) / nsplit;
+    fpc = (fpc + TILE_WARPS - 1) / TILE_WARPS * TILE_WARPS;
+    nsplit = (a.N + fpc - 1) / fpc;
+    void* args[] = {(void*)&a, (void*)&fpc};
+    FFCA_CK(cudaLaunchKernel(tf, dim3(unsigned(blocks), unsigned(nsplit)), dim3(TILE_F * TILE_WARPS), args, 0, s));
     count_launch();
     return FFCA_OK;
   }
