@@ -515,7 +515,10 @@ __global__ void __launch_bounds__(256) point_tile_big_kernel(const PointArgs a, 
       for (int b = 0; b < I; ++b) {
         const C2 pe = Ps[(x * I + b) * 32 + lane];
 #pragma unroll
-        for (int r = 0; r < FP; ++r) cmac_conj(t[r][b], pe, y[r][x]);
+        for (int r = 0; r < FP; ++r) {  // t += conj(p) y = p.x (y.x, y.y) + p.y (y.y, -y.x): two packed FMAs
+          t[r][b] = fma2(y[r][x], bc2<R>(pe.x), t[r][b]);
+          t[r][b] = fma2(mk<C2, R>(y[r][x].y, -y[r][x].x), bc2<R>(pe.y), t[r][b]);
+        }
       }
     R w[FP][I];
 #pragma unroll
@@ -553,7 +556,7 @@ __global__ void __launch_bounds__(256) point_tile_big_kernel(const PointArgs a, 
           const R aa = v[r] * l;
           const R iw = rcp(w[r][i]);
           const R g = aa * iw;
-          m[r][i] = mk<C2, R>(g * t[r][i].x, g * t[r][i].y);
+          m[r][i] = fma2(t[r][i], bc2<R>(g), mk<C2, R>(R(0), R(0)));
           ph[r][i] = fmax(aa * (w[r][i] - aa) * iw, R(0));
         }
       }
@@ -596,9 +599,9 @@ __global__ void __launch_bounds__(256) point_tile_big_kernel(const PointArgs a, 
           for (int b = 0; b < I; ++b) {  // acc += Q[x][b] mu[b]
             const C2 q = Qs[(x * I + b) * 32 + lane];
 #pragma unroll
-            for (int r = 0; r < FP; ++r) {
-              acc[r].x = fma(q.x, m[r][b].x, fma(-q.y, m[r][b].y, acc[r].x));
-              acc[r].y = fma(q.x, m[r][b].y, fma(q.y, m[r][b].x, acc[r].y));
+            for (int r = 0; r < FP; ++r) {  // q mu = q.x (mu.x, mu.y) + q.y (-mu.y, mu.x)
+              acc[r] = fma2(m[r][b], bc2<R>(q.x), acc[r]);
+              acc[r] = fma2(mk<C2, R>(-m[r][b].y, m[r][b].x), bc2<R>(q.y), acc[r]);
             }
           }
 #pragma unroll
