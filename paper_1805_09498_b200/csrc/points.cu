@@ -613,6 +613,111 @@ __global__ void __launch_bounds__(256) point_tile_big_kernel(const PointArgs a, 
   }
 }
 
+// Back-transform x_j = Q mu_tilde_j, Q = P^-H (fastfca.py:258-273; the device pass of
+// wiener.mmse_images_fastfca, wiener.py:38-43), bin-tiled for every I <= 8: a CTA owns 32 consecutive
+// bins x a block of frames, Q of its bins sits in shared memory in the compute type (element-major,
+// bin fastest: conflict free), its 8 warps stride the frames.  Per (frame, source) a lane reads its
+// bin's I consecutive transformed means -- the warp's 32 runs are one contiguous piece of the
+// (U, J, N, F, I) array -- with the next source's means already in flight, and writes either
+// coalesced 32-bin rows of the (U, J, I, N, F) image planes or its I consecutive outputs.
+// (The untiled point_kernel re-read the fp64 Q from global memory per point and solved in fp64:
+// config-3 scale 3.05 ms, config-4 shape 11.98 ms.)
+template <typename R, int I>
+__global__ void __launch_bounds__(256) back_tile_kernel(const PointArgs a, int frames_per_cta) {
+  using C2 = typename Cpx<R>::T;
+  extern __shared__ __align__(16) unsigned char back_sm[];
+  C2* Qs = (C2*)back_sm;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int F = a.F, N = a.N, J = a.J;
+  const int ftiles = (F + 31) / 32;
+  const long long u = blockIdx.x / ftiles;
+  const int f0 = int(blockIdx.x % ftiles) * 32;
+  const int n_lo = blockIdx.y * frames_per_cta;
+  const int n_hi = n_lo + frames_per_cta < N ? n_lo + frames_per_cta : N;
+  const bool live = f0 + lane < F;
+  const int f = live ? f0 + lane : F - 1;
+  for (int e = threadIdx.x; e < 32 * I * I; e += blockDim.x) {
+    const int lb = e / (I * I), el = e % (I * I);
+    const int fb = f0 + lb < F ? f0 + lb : F - 1;
+    const double2 q = ((const double2*)a.Q)[(u * F + fb) * I * I + el];
+    Qs[el * 32 + lb] = mk<C2, R>(R(q.x), R(q.y));
+  }
+  __syncthreads();
+  const long long rowN = (long long)N * F;
+  const C2* __restrict__ mu = (const C2*)a.y + u * J * rowN * I;
+  C2* __restrict__ out = (C2*)a.out0 + u * J * rowN * I;
+  auto load = [&](int j, long long o, C2 (&m)[I]) {  // the lane's I consecutive means of source j at point o
+    const C2* src = mu + (j * rowN + o) * I;
+    if constexpr (sizeof(C2) == 8 && I % 2 == 0) {
+#pragma unroll
+      for (int i = 0; i < I; i += 2) {
+        const float4 t = reinterpret_cast<const float4*>(src)[i / 2];
+        m[i] = mk<C2, R>(R(t.x), R(t.y));
+        m[i + 1] = mk<C2, R>(R(t.z), R(t.w));
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < I; ++i) m[i] = src[i];
+    }
+  };
+#pragma unroll 1
+  for (int n = n_lo + wp; n < n_hi; n += 8) {
+    const long long o = (long long)n * F + f;
+    C2 cur[I], nxt[I];
+    load(0, o, cur);
+#pragma unroll 1
+    for (int j = 0; j < J; ++j) {
+      if (j + 1 < J) load(j + 1, o, nxt);
+      C2 x[I];
+#pragma unroll
+      for (int r = 0; r < I; ++r) {
+        C2 acc = mk<C2, R>(R(0), R(0));
+#pragma unroll
+        for (int b = 0; b < I; ++b) {  // acc += Q[r][b] mu[b] = q.x (mu.x, mu.y) + q.y (-mu.y, mu.x)
+          const C2 q = Qs[(r * I + b) * 32 + lane];
+          acc = fma2(cur[b], bc2<R>(q.x), acc);
+          acc = fma2(mk<C2, R>(-cur[b].y, cur[b].x), bc2<R>(q.y), acc);
+        }
+        x[r] = acc;
+      }
+      if (live) {
+        if (a.images_layout) {
+          C2* d = out + (long long)j * I * rowN + o;
+#pragma unroll
+          for (int r = 0; r < I; ++r) d[r * rowN] = x[r];
+        } else {
+          C2* d = out + (j * rowN + o) * I;
+          if constexpr (sizeof(C2) == 8 && I % 2 == 0) {
+#pragma unroll
+            for (int r = 0; r < I; r += 2)
+              reinterpret_cast<float4*>(d)[r / 2] = make_float4(float(x[r].x), float(x[r].y), float(x[r + 1].x), float(x[r + 1].y));
+          } else {
+#pragma unroll
+            for (int r = 0; r < I; ++r) d[r] = x[r];
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < I; ++i) cur[i] = nxt[i];
+    }
+  }
+}
+
+template <typename R>
+static void* back_tile_fn(int I) {
+  switch (I) {
+    case 1: return (void*)back_tile_kernel<R, 1>;
+    case 2: return (void*)back_tile_kernel<R, 2>;
+    case 3: return (void*)back_tile_kernel<R, 3>;
+    case 4: return (void*)back_tile_kernel<R, 4>;
+    case 5: return (void*)back_tile_kernel<R, 5>;
+    case 6: return (void*)back_tile_kernel<R, 6>;
+    case 7: return (void*)back_tile_kernel<R, 7>;
+    case 8: return (void*)back_tile_kernel<R, 8>;
+  }
+  return nullptr;
+}
+
 template <typename R, int MODE>
 static void* big_tile_fn(int I) {
   switch (I) {
@@ -716,6 +821,21 @@ int launch_points(int dtype, const PointArgs& a, cudaStream_t s) {
     nsplit = (a.N + fpc - 1) / fpc;
     void* args[] = {(void*)&a, (void*)&fpc};
     FFCA_CK(cudaLaunchKernel(tf, dim3(unsigned(blocks), unsigned(nsplit)), dim3(TILE_F * TILE_WARPS), args, 0, s));
+    count_launch();
+    return FFCA_OK;
+  }
+  if (a.mode == PM_BACK && a.I <= 8) {
+    void* tf = dtype == FFCA_C64 ? back_tile_fn<float>(a.I) : back_tile_fn<double>(a.I);
+    const size_t smem = size_t(32) * a.I * a.I * (dtype == FFCA_C64 ? 8 : 16);
+    const long long tiles = (long long)a.U * ((a.F + 31) / 32);
+    int nsplit = int((8LL * 148 + tiles - 1) / tiles);
+    if (nsplit > (a.N + 31) / 32) nsplit = (a.N + 31) / 32;
+    if (nsplit < 1) nsplit = 1;
+    int fpc = (a.N + nsplit - 1) / nsplit;
+    fpc = (fpc + 7) / 8 * 8;
+    nsplit = (a.N + fpc - 1) / fpc;
+    void* args[] = {(void*)&a, (void*)&fpc};
+    FFCA_CK(cudaLaunchKernel(tf, dim3(unsigned(tiles), unsigned(nsplit)), dim3(256), args, smem, s));
     count_launch();
     return FFCA_OK;
   }
