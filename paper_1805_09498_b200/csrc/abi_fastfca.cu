@@ -104,7 +104,7 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
     const bool fits2 = p.slab <= kSlabBudget && p.smem <= smem_optin;
     if (fits2 && t2 >= 128) {
       fill(1, 1, true);
-      p.threads = t2 / 2;
+      p.threads = (t2 / 2 + 31) / 32 * 32;  // whole warps (t2 = 160 ... 224 for 130 <= N <= 448 halves to 80 ... 112)
       LoopSmem L(I, J, JM, 1, p.NL, p.threads / 32, rsz, vf_mode, true, VMAX);
       p.L = L;
       p.smem = L.total;

@@ -88,6 +88,25 @@ def test_plan_introspection_without_device():
     assert out[0] == 1 and out[3] == 128
 
 
+@pytest.mark.skipif(not os.path.exists(LIB), reason="library not built")
+def test_every_plan_launches_whole_warps():
+    # the kernels shuffle with the full mask: a CTA whose thread count is not a multiple of 32 is a bug
+    # (complex128, 130 <= N <= 448 once planned 80..112-thread CTAs)
+    import numpy as np
+
+    from paper_1805_09498_b200 import _lib
+    lib = _lib.load()
+    out = np.zeros(8, np.int32)
+    for code in (_lib.C64, _lib.C128):
+        for I, J in ((1, 2), (2, 2), (3, 3), (4, 4), (3, 5), (6, 3), (8, 6)):
+            for N in list(range(1, 700, 9)) + [2000, 4000, 9375, 12000]:
+                for U in (1, 64):
+                    for lean in (0, 1):
+                        assert lib.ffca_plan_loop_ex(0, code, U, I, J, N, 513, _lib.VF_AUTO, lean,
+                                                     out.ctypes.data_as(_lib._ip)) == 0
+                        assert out[3] >= 32 and out[3] % 32 == 0, (code, I, J, N, U, lean, out[:6])
+
+
 def test_product_has_no_cpu_fallback(monkeypatch):
     """Without a device the product path must fail loudly, never compute on the CPU."""
     import numpy as np
