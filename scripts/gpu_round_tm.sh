@@ -12,3 +12,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:ffca
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:ffca_loop -c 1 -f -o gpurun_out/r2tm_c2 python scripts/run_once.py 2 > gpurun_out/r2tm_c2.log 2>&1; echo "c2 rc=$?"
 timeout 300 python scripts/config_sweep.py > gpurun_out/r2tm_config_sweep.log 2>&1; echo "sweep rc=$?"
 tail -3 gpurun_out/r2tm_gputest.log
+timeout 300 python scripts/pipeline_bench.py > gpurun_out/r2tm_pipeline_bench.json 2> gpurun_out/r2tm_pipeline_bench.err; echo "pipeline rc=$?"
+for c in 3 2 4; do CFG=$c timeout 200 python scripts/points_bench.py c64; CFG=$c timeout 200 python scripts/back_bench.py; done > gpurun_out/r2tm_output_kernels.log 2>&1; echo "outputs rc=$?"
