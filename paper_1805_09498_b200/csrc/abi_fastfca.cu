@@ -111,7 +111,7 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
       if (p.slab <= kSlabBudget && p.smem <= smem_optin) return FFCA_OK;
     }
   }
-  // complex64, I = J = 3, lean loop, N <= 640: 4-bin CTAs of 128 threads (32 per bin, 10 frame pairs
+  // complex64, I = J = 3, N <= 640: 4-bin CTAs of 128 threads (32 per bin, 10 frame pairs
   // per thread) with the y records in tensor memory -- 16 bins per SM instead of the 8 that shared
   // memory alone holds, at the same 16 warps.
   // Worth it from one full wave of 16 bins per SM on (measured on B200, config-3 shape: 1 / 2 / 4 / 8
@@ -119,7 +119,9 @@ static int plan_loop(int dtype, int I, int J, int N, long long total_bins, int v
   // shared-memory plan); FFCA_TMEM_MIN_BINS overrides the threshold (tests use 0).
   long long tm_min_bins = 16LL * nsm;
   if (const char* e = getenv("FFCA_TMEM_MIN_BINS")) tm_min_bins = atoll(e);
-  if (dtype == FFCA_C64 && I == 3 && J == 3 && G0 == 4 && fast && vf_mode != 2 && N <= 640 && total_bins >= tm_min_bins &&
+  // (the loop with the likelihood record / inner iterations runs the same plan: 24.3 -> 22.5 ms at the
+  // config-3 scale with the likelihood recorded; only a full floor array needs the shared-memory plans)
+  if (dtype == FFCA_C64 && I == 3 && J == 3 && G0 == 4 && vf_mode != 2 && N <= 640 && total_bins >= tm_min_bins &&
       !getenv("FFCA_NO_TMEM")) {
     fill(4, 1, true);
     p.threads = 128;

@@ -1118,10 +1118,16 @@ struct PointWork {
     const int sy = rstep * 2 * RS, sv = rstep * 2 * JS;
     const int n = nfull + (part ? 1 : 0);
 #pragma unroll 1
-    for (int k = 0; k < n; ++k, yp += sy, vp += sv) {
+    for (int k = 0; k < (TM ? nrec : n); ++k, yp += sy, vp += sv) {
       const bool half = part && k == n - 1;
       C2 ya[I], yb[I], v2[JM], q2[I], iw2[I], w2[I];
-      load_pair(yp, vp, ya, yb, v2);
+      if constexpr (TM) {
+        tm_load_pair(k, ya, yb);  // warp-collective: every lane, every record
+        if (k >= n) continue;
+        load_v_pair(vp, v2);
+      } else {
+        load_pair(yp, vp, ya, yb, v2);
+      }
       q_pair(ya, yb, q2);
       iw_pair(v2, iw2, w2);
 #pragma unroll
@@ -1299,8 +1305,8 @@ __global__ void __launch_bounds__(256) slab_pack_kernel(const PackArgs a) {
 // (instruction cache) and lighter on registers.  The launcher picks it when a call allows.
 template <typename R, int I, int JT, int G, bool RES, bool FAST = false, bool TM = false>
 __global__ void __launch_bounds__(TM ? 128 : 256, (TM && I == 3) ? 4 : ((I == 4 || (I > 4 && RES)) ? 1 : 2)) ffca_loop_kernel(const LoopArgs a) {
-  static_assert(!TM || (FAST && RES && sizeof(R) == 4 && ((G == 4 && I == 3) || (G == 1 && I == 4))),
-                "tensor-memory plans: the lean complex64 loop, 4-bin CTAs at I = 3 or cluster CTAs at I = 4");
+  static_assert(!TM || (RES && sizeof(R) == 4 && ((G == 4 && I == 3) || (FAST && G == 1 && I == 4))),
+                "tensor-memory plans: complex64, 4-bin CTAs at I = 3 (lean or full loop) or lean cluster CTAs at I = 4");
   using C2 = typename Cpx<R>::T;
   constexpr int JM = JT > 0 ? JT : 8;
   constexpr int IC = Shape<I, JM>::IC, NCH = Shape<I, JM>::NCH, NB = Shape<I, JM>::NB;

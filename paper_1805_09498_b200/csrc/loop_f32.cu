@@ -11,7 +11,10 @@ using LoopFn = void (*)(const LoopArgs);
 template <int I, int J>
 static LoopFn hot(int G, bool res, bool fast, bool tm) {
   if constexpr (I == 3 && J == 3)
-    if (tm) return (G == 4 && res && fast) ? (LoopFn)ffca_loop_kernel<float, 3, 3, 4, true, true, true> : nullptr;
+    if (tm)
+      return !(G == 4 && res) ? nullptr
+             : fast           ? (LoopFn)ffca_loop_kernel<float, 3, 3, 4, true, true, true>
+                              : (LoopFn)ffca_loop_kernel<float, 3, 3, 4, true, false, true>;
   if constexpr (I == 4 && J == 4)
     if (tm) return (G == 1 && res && fast) ? (LoopFn)ffca_loop_kernel<float, 4, 4, 1, true, true, true> : nullptr;
   if constexpr (I <= 4) {

@@ -62,8 +62,11 @@ def test_plan_introspection_without_device():
     # ... from one wave of 16 bins per SM on; a single mixture keeps 2 bins per CTA in shared memory
     assert lib.ffca_plan_loop_ex(0, _lib.C64, 1, 3, 3, 626, 513, _lib.VF_AUTO, 1, out8.ctypes.data_as(_lib._ip)) == 0
     assert out8[0] == 2 and out8[3] == 128 and out8[6] == 0
-    # ... the loop with the likelihood record keeps 2 bins per 128-thread CTA in shared memory
+    # ... the loop with the likelihood record runs the same plan; a full floor array (vf_mode 2) needs the
+    # shared-memory plan (2 bins per 128-thread CTA)
     assert lib.ffca_plan_loop_ex(0, _lib.C64, 256, 3, 3, 626, 513, _lib.VF_AUTO, 0, out8.ctypes.data_as(_lib._ip)) == 0
+    assert out8[0] == 4 and out8[3] == 128 and out8[6] == 1
+    assert lib.ffca_plan_loop_ex(0, _lib.C64, 256, 3, 3, 626, 513, 2, 0, out8.ctypes.data_as(_lib._ip)) == 0
     assert out8[0] == 2 and out8[3] == 128 and out8[4] == 1 and out8[6] == 0
     # ... and so do bins longer than the 640 frames a CTA's 128 columns hold
     assert lib.ffca_plan_loop_ex(0, _lib.C64, 256, 3, 3, 642, 513, _lib.VF_AUTO, 1, out8.ctypes.data_as(_lib._ip)) == 0

@@ -104,18 +104,19 @@ def test_small_batches_keep_the_shared_memory_plan():
 
 
 def test_plans_that_do_not_use_tensor_memory():
-    # bins longer than 640 frames, the loop with the likelihood record, and the opt-out switch keep
-    # the shared-memory plans; all agree with the tensor-memory plan to fp32 regrouping error
+    # bins longer than 640 frames and the opt-out switch keep the shared-memory plans, which agree with
+    # the tensor-memory plan to fp32 regrouping error; the loop with the likelihood record runs the
+    # tensor-memory plan too and leaves the estimates of the plain loop unchanged
     assert plan8(1, 6, 642)[6] == 0
-    assert plan8(1, 6, 200, lean=0)[6] == 0
+    assert plan8(1, 6, 200, lean=0)[6] == 1
     args = batch(2, 6, 200, 17)
     tm = fastfca.run_fastfca_batch(*args, iterations=5)
     full = fastfca.run_fastfca_batch(*args, iterations=5, record_likelihood=True)
     os.environ["FFCA_NO_TMEM"] = "1"
-    assert plan8(2, 6, 200)[6] == 0
+    assert plan8(2, 6, 200)[6] == 0 and plan8(2, 6, 200, lean=0)[6] == 0
     off = fastfca.run_fastfca_batch(*args, iterations=5)
     for a, b, c in zip(tm[:3], full[:3], off[:3]):
-        assert rel(a, b) <= 1e-5 and rel(a, c) <= 1e-5
+        assert rel(a, b) <= 1e-6 and rel(a, c) <= 1e-5
     long_args = batch(1, 6, 642, 23)
     P = fastfca.run_fastfca_batch(*long_args, iterations=3)[0]
     assert np.isfinite(P).all()
@@ -153,3 +154,25 @@ def test_cluster_tmem_plan_i4(N, C):
         assert np.array_equal(a, c)
         assert rel(a, b) <= 1e-5
         assert rel(a[0], want) <= 1e-4
+
+
+@pytest.mark.parametrize("F,N,K", [(6, 151, 1), (5, 640, 1), (7, 33, 2), (4, 2, 1)])
+def test_tmem_plan_full_loop_likelihood(F, N, K):
+    # the loop with the likelihood record (and inner iterations) on the tensor-memory plan: state and
+    # every recorded likelihood against the oracle, and against the shared-memory plan
+    assert plan8(1, F, N, lean=0)[6] == 1
+    y, P0, lam0, v0, _ = mixture(77 + N, 3, 3, F, N, 4, 0.0)
+    a32 = (y.astype(np.complex64)[None], P0.astype(np.complex64)[None], lam0.astype(np.float32)[None],
+           v0.astype(np.float32)[None])
+    T = 4
+    P, lam, v, ll = fastfca.run_fastfca_batch(*a32, iterations=T, inner_iterations=K, record_likelihood=True)
+    os.environ["FFCA_NO_TMEM"] = "1"
+    Ps, lams, vs, lls = fastfca.run_fastfca_batch(*a32, iterations=T, inner_iterations=K, record_likelihood=True)
+    assert rel(P, Ps) <= 1e-5 and rel(v, vs) <= 1e-5
+    assert np.max(np.abs(ll - lls) / np.abs(lls)) <= 1e-6
+    if N > 3:  # (fewer frames than channels: singular B_i, not an oracle case)
+        ref = ffr.run_fastfca(y, P0, lam0, v0, iterations=T, inner_iterations=K, record_likelihood=True, stats=False)
+        assert rel(P[0], ref.P) <= 1e-4 and rel(lam[0], ref.lam) <= 1e-4 and rel(v[0], ref.v) <= 1e-4
+        want = np.array([ref.loglik_init] + list(ref.loglik_after_em) + list(ref.loglik_after_p))
+        got = np.array([ll[0, 0]] + list(ll[0, 1:2 * T + 1:2]) + list(ll[0, 2:2 * T + 1:2]))
+        assert np.max(np.abs(got - want) / np.abs(want)) <= 1e-4
