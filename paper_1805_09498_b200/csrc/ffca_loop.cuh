@@ -843,7 +843,7 @@ struct PointWork {
       const int nf = min(32, NLr - 32 * c);
       const C2* rec = ys + (32 * c + h) * RS;
       const R* wq = wbuf + h * IWS;
-#pragma unroll 2
+#pragma unroll 8
       for (int f = h; f < nf; f += 2, rec += 2 * RS, wq += 2 * IWS) {
         // units 0..15 are complex entries whenever I >= 7 (NCX >= 16): no diagonal selects
         const C2 z0 = unit_z(rec, ua[0], ub[0], Shape<I, JM>::NCX >= 16 ? false : dg[0]);
