@@ -575,7 +575,7 @@ struct PointWork {
     const C2* yp = ys + rec0 * RS;
     R* vp = vs + rec0 * JS;
     const R* fp = vfs + rec0 * JS;
-#pragma unroll 1
+#pragma unroll 2
     for (int k = 0; k < npts; k += 2, yp += 2 * st * RS, vp += 2 * st * JS, fp += 2 * st * JS) {
       const bool two = k + 1 < npts;
       const int o1 = two ? st : 0;  // a lone last frame is computed twice, used once
