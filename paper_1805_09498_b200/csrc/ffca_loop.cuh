@@ -933,16 +933,18 @@ struct PointWork {
     }
   }
 
-  template <bool REC, bool VF2, bool PART>
+  template <bool REC, bool VF2, int PART>
   __device__ __forceinline__ void pairA(const C2* yp, R* vp, const R* fp, C2 (&s0)[JM], C2 (&s1)[JM][I], C2& lacc,
                                         const R vfl_b) const {
     C2 ya[I], yb[I];
     load_y_pair(yp, ya, yb);
     pairA_core<REC, VF2, PART>(ya, yb, vp, fp, s0, s1, lacc, vfl_b);
   }
-  template <bool REC, bool VF2, bool PART>
+  // PART: 0 full pair, 1 half pair (frame b is padding), 2 decided at run time by `half`
+  template <bool REC, bool VF2, int PART>
   __device__ __forceinline__ void pairA_core(const C2 (&ya)[I], const C2 (&yb)[I], R* vp, const R* fp, C2 (&s0)[JM],
-                                             C2 (&s1)[JM][I], C2& lacc, const R vfl_b) const {
+                                             C2 (&s1)[JM][I], C2& lacc, const R vfl_b, bool half = false) const {
+    const bool isp = PART == 2 ? half : (PART == 1);
     C2 v2[JM];
     load_v_pair(vp, v2);
     C2 q2[I], iw2[I], w2[I], d2[I];
@@ -953,7 +955,7 @@ struct PointWork {
       d2[i] = mul2(fma2(q2[i], iw2[i], bc2<R>(R(-1))), iw2[i]);  // d = q / w^2 - 1 / w
       if constexpr (REC)
         lacc = add2(lacc, mk<C2, R>(flog(w2[i].x) + q2[i].x * iw2[i].x,
-                                    PART ? R(0) : flog(w2[i].y) + q2[i].y * iw2[i].y));
+                                    isp ? R(0) : flog(w2[i].y) + q2[i].y * iw2[i].y));
     }
 #pragma unroll
     for (int j = 0; j < JM; ++j) {
@@ -966,9 +968,12 @@ struct PointWork {
         // v' = max(v - v^2 (r1 - r2) / I, floor)   (fastfca.py:336-337)
         C2 vn = fma2(sd, mul2(mul2(v2[j], v2[j]), bc2<R>(invI)), v2[j]);
         vn = mk<C2, R>(fmax(vn.x, fl.x), fmax(vn.y, fl.y));
-        if constexpr (PART) {
+        if constexpr (PART == 1) {
           *(C2*)(vp + 2 * j) = mk<C2, R>(vn.x, R(0));  // the padding frame keeps v = 0
           vn.y = R(1);
+        } else if constexpr (PART == 2) {
+          *(C2*)(vp + 2 * j) = mk<C2, R>(vn.x, isp ? R(0) : vn.y);
+          vn.y = isp ? R(1) : vn.y;
         } else {
           *(C2*)(vp + 2 * j) = vn;
         }
@@ -999,8 +1004,8 @@ struct PointWork {
       for (int k = 0; k < nrec; ++k, vp += sv, fp += sv) {
         C2 ya[I], yb[I];
         tm_load_pair(k, ya, yb);
-        if (k < nfull) pairA_core<REC, VF2, false>(ya, yb, vp, fp, s0, s1, lacc, vfl_b);
-        else if (part && k == nfull) pairA_core<REC, VF2, true>(ya, yb, vp, fp, s0, s1, lacc, vfl_b);
+        // one body for full and half pairs (the half pair selects at run time): half the loop's code
+        if (k < nfull + (part ? 1 : 0)) pairA_core<REC, VF2, 2>(ya, yb, vp, fp, s0, s1, lacc, vfl_b, k == nfull);
       }
     } else {
 #pragma unroll 1
@@ -1085,8 +1090,12 @@ struct PointWork {
       for (int k = 0; k < nrec; ++k, vp += sv) {
         C2 ya[I], yb[I];
         tm_load_pair(k, ya, yb);
-        if (k < nfull) pairB_core<REC, false>(ya, yb, vp, ac, ad, lacc);
-        else if (part && k == nfull) pairB_core<REC, true>(ya, yb, vp, ac, ad, lacc);
+        if constexpr (REC) {
+          if (k < nfull) pairB_core<REC, false>(ya, yb, vp, ac, ad, lacc);
+          else if (part && k == nfull) pairB_core<REC, true>(ya, yb, vp, ac, ad, lacc);
+        } else {  // without the likelihood a half pair's zero padding frame adds nothing: one body
+          if (k < nfull + (part ? 1 : 0)) pairB_core<REC, false>(ya, yb, vp, ac, ad, lacc);
+        }
       }
     } else {
 #pragma unroll 1
